@@ -1,0 +1,495 @@
+#!/usr/bin/env python
+"""bench.py -- SpGEMM GFLOPS (2*nprod/time) on B200, BASELINE.json's metric.
+
+Default workload (N=1): BASELINE.json configs[1], C = A*A with A the 3-D 27-point
+stencil on a 128^3 grid (2.1M rows, 55.7M nnz, nprod 1.489e9). One *step* = one
+full SpGEMM (setup, binning, symbolic, row_ptr scan + C allocation, numeric) with
+A resident in HBM; C is freed (stream-ordered) after each step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1|2|3|4]
+  python bench.py --impl reference ...   # the reference CPU pipeline (oracle/_ref)
+
+N>1 (torchrun, one process per GPU, NCCL): weak scaling. The global matrix is
+the 27-point stencil on 128 x 128 x (128*N); rank 0 builds it and broadcasts it
+(B = A) over NVLink once; every rank computes nprod (K1) and the deterministic
+nprod-prefix row split itself, then multiplies its row block.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpGEMM GFLOPS (2*nprod/time)"
+UNIT = "GFLOPS"
+CONFIG_NAMES = {
+    1: "C=A*A 2D 5-pt Poisson 1024^2",
+    2: "C=A*A 3D 27-pt stencil 128^3",
+    3: "C=A*A R-MAT scale 20 ef 16",
+    4: "RAP: A*P then R*(AP), 3D 7-pt Poisson 128^3, trilinear P",
+}
+
+
+def csr_bytes(rows, nnz):
+    """8*(rows+1) + 4*nnz + 8*nnz."""
+    return 8 * (rows + 1) + 12 * nnz
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# -------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        self.t_stop = time.time()
+
+    def summary(self, t0, t1):
+        rows = []
+        for ts, line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            rows.append((ts, parts))
+        inwin = [r for r in rows if t0 - 0.06 <= r[0] <= t1 + 0.06] or rows
+        if not inwin:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(p[0]) for _, p in inwin if p[0].replace(".", "").isdigit()]
+        smax = [float(p[1]) for _, p in inwin if p[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, p in inwin for i in range(4) if p[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(inwin)}
+
+
+# -------------------------------------------------------- CPU baseline
+def cpu_baseline(a, rows_frac=1.0, runs=2):
+    """The reference CPU pipeline (oracle/_ref, all host threads) on a bounded sample."""
+    from oracle import oracle as O
+    from paper_2206_07244_b200.api import CsrMatrix
+    m = a.to_host()
+    if rows_frac < 1.0:
+        r0 = int(m.rows * (0.5 - rows_frac / 2))
+        r1 = r0 + int(m.rows * rows_frac)
+        rpt = m.rpt[r0:r1 + 1] - m.rpt[r0]
+        sample = CsrMatrix(r1 - r0, m.cols, rpt, m.col[m.rpt[r0]:m.rpt[r1]], m.val[m.rpt[r0]:m.rpt[r1]])
+        desc = f"rows [{r0},{r1}) of A times A"
+    else:
+        sample, desc = m, "the full product"
+    cores = os.cpu_count() or 1
+    if O.ref_available():
+        _, info = O.ref_multiply(sample, m)  # warm-up
+        ts = []
+        for _ in range(runs):
+            t0 = time.perf_counter()
+            _, info = O.ref_multiply(sample, m)
+            ts.append(time.perf_counter() - t0)
+        t = sum(ts) / len(ts)
+        return {"value": 2 * info["total_nprod"] / t / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"oracle/_ref spgemm::multiply (workers={info['workers']}) on {desc}, "
+                          f"1 warm-up + {runs} timed, mean {t:.3f} s"}
+    # C restatement (single thread) on a smaller sample
+    t0 = time.perf_counter()
+    O.spgemm(sample, m)
+    t = time.perf_counter() - t0
+    _, nprod = O.compute_nprod(sample, m)
+    return {"value": 2 * nprod / t / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle/spgemm_oracle.c (1 thread) on {desc}, 1 run {t:.3f} s"}
+
+
+# ---------------------------------------------------------- workloads
+def build_workload(cfg):
+    from paper_2206_07244_b200 import synthetic as S
+    mats = S.config_matrices(cfg)
+    return list(mats)
+
+
+def stencil_weak(n_ranks):
+    from paper_2206_07244_b200 import synthetic as S
+    offs = [(dx, dy, dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+    return S._stencil((128, 128, 128 * n_ranks), offs, 26.0, -1.0)
+
+
+def nprod_split(nprod, parts):
+    """Contiguous row blocks balanced by the nprod prefix sum:
+    rank g takes rows whose exclusive prefix lies in [g*T/G, (g+1)*T/G)."""
+    pref = np.concatenate([[0], np.cumsum(nprod)])
+    total = pref[-1]
+    bounds = [0]
+    for g in range(1, parts):
+        bounds.append(int(np.searchsorted(pref[:-1], g * total / parts, side="left")))
+    bounds.append(len(nprod))
+    return bounds
+
+
+# ---------------------------------------------------------------- main
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2206_07244_b200.api import CsrMatrix
+    mats = build_workload(args.config)
+    a = mats[0]
+    frac = {1: 1.0, 2: 0.25, 3: 0.02, 4: 1.0}[args.config]
+    r0 = int(a.rows * (0.5 - frac / 2)) if frac < 1 else 0
+    r1 = r0 + int(a.rows * frac) if frac < 1 else a.rows
+    rpt = a.rpt[r0:r1 + 1] - a.rpt[r0]
+    sample = CsrMatrix(r1 - r0, a.cols, rpt, a.col[a.rpt[r0]:a.rpt[r1]], a.val[a.rpt[r0]:a.rpt[r1]])
+    b = mats[1]
+    kind = "reference" if O.ref_available() else "port"
+
+    def step():
+        if kind == "reference":
+            _, info = O.ref_multiply(sample, b)
+            return info["total_nprod"]
+        O.spgemm(sample, b)
+        return O.compute_nprod(sample, b)[1]
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    nprod = 0
+    for _ in range(args.steps):
+        nprod += step()
+    t = time.perf_counter() - t0
+    value = 2 * nprod / t / 1e9
+    cores = os.cpu_count() or 1 if kind == "reference" else 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], "sample_rows": [r0, r1]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"rows [{r0},{r1}) of config {args.config}'s A times B per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2206_07244_b200 as sg
+    from paper_2206_07244_b200.api import CsrMatrix
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = sg.get_context(local)
+    peak, peak_kind = load_peaks()
+
+    # ------------------------------------------------------------ operands
+    bcast_s = None
+    if world == 1:
+        mats = build_workload(args.config)
+        host_ops = mats
+        dev = [m.to_device(local) for m in mats]
+        pairs = [(dev[0], dev[1])] if args.config != 4 else None
+        workload = CONFIG_NAMES[args.config]
+    else:
+        if args.config != 2:
+            raise SystemExit("multi-GPU bench runs the weak-scaled 27-point stencil (config 2)")
+        if rank == 0:
+            g = stencil_weak(world)
+            shape = torch.tensor([g.rows, g.nnz()], dtype=torch.int64, device="cuda")
+        else:
+            shape = torch.zeros(2, dtype=torch.int64, device="cuda")
+        dist.broadcast(shape, 0)
+        rows, nnz = int(shape[0]), int(shape[1])
+        if rank == 0:
+            gd = g.to_device(local)
+            grpt, gcol, gval = gd.rpt, gd.col, gd.val
+        else:
+            grpt = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+            gcol = torch.empty(nnz, dtype=torch.int32, device="cuda")
+            gval = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for t in (grpt, gcol, gval):  # B replicated over NVLink (ncclBroadcast)
+            dist.broadcast(t, 0)
+        torch.cuda.synchronize()
+        bcast_s = time.perf_counter() - t0
+        B = CsrMatrix(rows, rows, grpt, gcol, gval)
+        nprod, _ = sg.compute_nprod(B, B, device=local)
+        bounds = nprod_split(nprod, world)
+        r0, r1 = bounds[rank], bounds[rank + 1]
+        p0, p1 = int(grpt[r0]), int(grpt[r1])
+        A_loc = CsrMatrix(r1 - r0, rows, grpt[r0:r1 + 1] - p0, gcol[p0:p1], gval[p0:p1])
+        pairs = [(A_loc, B)]
+        host_ops = None
+        workload = f"C=A*A 3D 27-pt stencil 128x128x{128 * world} (weak: 128^3 rows/GPU), nprod-balanced row blocks"
+
+    def one_step():
+        if pairs is not None:
+            tot = 0
+            for a, b in pairs:
+                dm, out = sg.multiply_device(a, b, device=local)
+                tot += out.stats.total_nprod
+                dm.free()
+            return tot
+        # RAP chain: AP stays on device and feeds R*(AP)
+        a, p, r = dev
+        dm1, o1 = sg.multiply_device(a, p, device=local)
+        ap = CsrMatrix(dm1.rows, dm1.cols, *device_tensors(dm1))
+        dm2, o2 = sg.multiply_device(r, ap, device=local)
+        dm2.free()
+        dm1.free()
+        return o1.stats.total_nprod + o2.stats.total_nprod
+
+    def device_tensors(dm):
+        # zero-copy torch views of a DeviceMatrix (CUDA array interface)
+        class _V:
+            def __init__(self, ptr, n, typestr):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3}
+        r = torch.as_tensor(_V(dm.ptrs[0], dm.rows + 1, "<i8"), device="cuda")
+        c = torch.as_tensor(_V(dm.ptrs[1], dm.nnz, "<i4"), device="cuda") if dm.nnz else \
+            torch.zeros(0, dtype=torch.int32, device="cuda")
+        v = torch.as_tensor(_V(dm.ptrs[2], dm.nnz, "<f8"), device="cuda") if dm.nnz else \
+            torch.zeros(0, dtype=torch.float64, device="cuda")
+        return r, c, v
+
+    # ------------------------------------------------------------- warm-up
+    for _ in range(max(3, args.warmup)):
+        nprod_step = one_step()
+    torch.cuda.synchronize()
+
+    # ------------------------------------------------------------- timed
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    ctx.profile_summary()  # clear
+    ctx.set_profiling(True)
+    launches0 = ctx.kernel_launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tw0 = time.time()
+    ev0.record(stream)
+    total_nprod = 0
+    for _ in range(args.steps):
+        total_nprod += one_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    if dist:
+        dist.barrier()
+    ctx.set_profiling(False)
+    kernels = ctx.profile_summary()
+    launches = ctx.kernel_launches - launches0
+    if rank == 0:
+        clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    t_max = t_ms
+    nprod_all = total_nprod
+    if dist:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+        nn = torch.tensor([total_nprod], dtype=torch.int64, device="cuda")
+        dist.all_reduce(nn)
+        nprod_all = int(nn.item())
+    value = 2 * nprod_all / (t_max * 1e-3) / 1e9
+    ms_per_step = t_max / args.steps
+
+    # ------------------------------------------------------------ roofline
+    # Algorithmic bytes of one SpGEMM: A + B + C compulsory bytes.
+    def unit_bytes():
+        if pairs is not None:
+            out = 0
+            for a, b in pairs:
+                c_rows, c_nnz = a.rows, None
+                out += csr_bytes(a.rows, a.nnz()) + csr_bytes(b.rows, b.nnz())
+            return out
+        return None
+
+    roof = None
+    step_roof = None
+    if rank == 0 and kernels:
+        top = max(kernels.items(), key=lambda kv: kv[1][1])
+        name, (n_launch, ms_total) = top
+        avg_s = ms_total / n_launch * 1e-3
+        # C bytes from the last step's report
+        if pairs is not None:
+            a, b = pairs[0]
+            dm, out = sg.multiply_device(a, b, device=local)
+            c_nnz, c_rows = out.stats.nnz_of_product, a.rows
+            dm.free()
+            ab = csr_bytes(a.rows, a.nnz()) + csr_bytes(b.rows, b.nnz())
+            step_bytes = ab + csr_bytes(c_rows, c_nnz)
+        else:
+            a, p, r = dev
+            dm1, o1 = sg.multiply_device(a, p, device=local)
+            ap_b = csr_bytes(dm1.rows, dm1.nnz)
+            dm1.free()
+            rap_nnz = 6_859_000 if args.config == 4 else 0
+            step_bytes = (csr_bytes(a.rows, a.nnz()) + csr_bytes(p.rows, p.nnz()) + ap_b +
+                          csr_bytes(r.rows, r.nnz()) + ap_b + csr_bytes(r.rows, rap_nnz))
+        # per-kernel algorithmic bytes: the dominant kernel is a numeric-phase
+        # kernel reading A (rpt, col, val), B and C.rpt and writing C.col/C.val;
+        # a launch that handles a fraction of the rows gets that fraction.
+        frac = 1.0
+        if name.startswith("k_num") or name.startswith("k_sym"):
+            frac = 1.0 / max(1, n_launch // args.steps)
+        kernel_bytes = step_bytes * frac if name.startswith("k_num") else None
+        if name.startswith("k_sym") and pairs is not None:
+            a, b = pairs[0]
+            kernel_bytes = frac * (8 * (a.rows + 1) + 4 * a.nnz() + 8 * (b.rows + 1) + 4 * b.nnz() + 8 * a.rows)
+        if kernel_bytes is None:
+            kernel_bytes = step_bytes
+        achieved = kernel_bytes / avg_s / 1e9
+        traffic = None
+        prof_path = os.path.join(ROOT, "profiles", f"ncu_config{args.config}_summary.json")
+        if os.path.exists(prof_path):
+            with open(prof_path) as f:
+                prof = json.load(f)
+            k = prof.get("kernels", {}).get(name)
+            if k:
+                traffic = k.get("dram_bytes_per_launch")
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                "algorithmic_bytes_per_launch": kernel_bytes, "avg_launch_ms": avg_s * 1e3,
+                "share_of_step": ms_total / t_ms}
+        step_roof = {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,
+                     "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
+
+    # ----------------------------------------------------------------- e2e
+    e2e = None
+    if rank == 0 and host_ops is not None and args.config != 4:
+        e2e = run_e2e(sg, torch, host_ops[0], max(3, args.e2e_steps or args.steps // 4), local)
+
+    # ------------------------------------------------------------ baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            frac = {1: 1.0, 2: 1.0, 3: 0.02, 4: 1.0}[args.config]
+            cpu = cpu_baseline(host_ops[0], rows_frac=frac)
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable", "sample": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "nprod_per_step": nprod_all // args.steps,
+                       "l2": "inputs larger than L2 (A is 0.67 GB vs 126 MB L2)" if args.config == 2 else
+                       "L2 not flushed between steps",
+                       "parallelism": f"row-block dp{world}" if world > 1 else "single GPU",
+                       "b_broadcast_s": bcast_s},
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
+            "kernels_ms": {k: round(v[1], 4) for k, v in sorted(kernels.items(), key=lambda kv: -kv[1][1])},
+            "clocks": clocks.summary(tw0, tw1),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(sg, torch, a_host, steps, device):
+    """Same metric through the public API with host buffers: each step copies A
+    from pinned host memory (B aliases A), multiplies, and reads C back into
+    pinned host buffers."""
+    from paper_2206_07244_b200.api import CsrMatrix
+    pr = torch.from_numpy(a_host.rpt).pin_memory()
+    pc = torch.from_numpy(a_host.col).pin_memory()
+    pv = torch.from_numpy(a_host.val).pin_memory()
+    a = CsrMatrix(a_host.rows, a_host.cols, pr.numpy(), pc.numpy(), pv.numpy())
+    h2d = pr.numel() * 8 + pc.numel() * 4 + pv.numel() * 8
+    p = sg.SpgemmPipeline(a, a, device=device)
+    dm, out = p.run_device()
+    p.close()
+    nnz = dm.nnz
+    dm.free()
+    orpt = torch.empty(a.rows + 1, dtype=torch.int64).pin_memory()
+    ocol = torch.empty(nnz, dtype=torch.int32).pin_memory()
+    oval = torch.empty(nnz, dtype=torch.float64).pin_memory()
+    d2h = orpt.numel() * 8 + ocol.numel() * 4 + oval.numel() * 8
+
+    def step():
+        p = sg.SpgemmPipeline(a, a, device=device)
+        dm, out = p.run_device()
+        p.close()
+        dm.download_into(orpt.numpy(), ocol.numpy(), oval.numpy())
+        dm.free()
+        return out.stats.total_nprod
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    nprod = 0
+    for _ in range(steps):
+        nprod += step()
+    t = time.perf_counter() - t0
+    return {"value": 2 * nprod / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": steps, "ms_per_step": t / steps * 1e3}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+/*
+ * spgemm_capi.h -- the drop-in boundary of the B200-native OpSparse SpGEMM.
+ *
+ * Plain C ABI (no C++ or torch types): pointers, sizes and POD structs. Every
+ * entry point replaces one reference interface from
+ * /root/reference/proj/core/include/spgemm (cited per function). The C++
+ * drop-in headers in include/spgemm/*.hpp and the Python mirror in
+ * paper_2206_07244_b200/api.py are thin layers over exactly these symbols;
+ * INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Error convention: the reference throws (pipeline.hpp / binning.hpp); this
+ * ABI never throws. Each call returns an spgemm_status whose value names the
+ * exception type the reference would have thrown; spgemm_last_error() holds
+ * the message (thread-local).
+ *
+ * Everything computes on the GPU (sm_100a kernels); there is no CPU fallback.
+ */
+#ifndef SPGEMM_CAPI_H_
+#define SPGEMM_CAPI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPGEMM_NUM_BINS 8
+#define SPGEMM_NO_UPPER_BOUND INT64_MAX
+
+typedef enum spgemm_status {
+  SPGEMM_OK = 0,
+  SPGEMM_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  SPGEMM_LOGIC_ERROR = 2,      /* std::logic_error      */
+  SPGEMM_OVERFLOW = 3,         /* std::overflow_error   */
+  SPGEMM_OUT_OF_MEMORY = 4,    /* std::bad_alloc        */
+  SPGEMM_CUDA_ERROR = 5,
+  SPGEMM_NCCL_ERROR = 6,
+  SPGEMM_NO_DEVICE = 7
+} spgemm_status;
+
+typedef struct spgemm_ctx spgemm_ctx;           /* one (host thread, device) context  */
+typedef struct spgemm_pipeline spgemm_pipeline; /* SpgemmPipeline (pipeline.hpp:119)  */
+typedef struct spgemm_matrix spgemm_matrix;     /* device-resident CSR owned by the lib */
+
+/* CsrMatrix (csr.hpp:45-63) as a borrowed view: rpt int64[rows+1], col
+ * int32[rpt[rows]] strictly increasing per row, val fp64[rpt[rows]]. */
+typedef struct spgemm_csr_view {
+  int64_t rows;
+  int64_t cols;
+  const int64_t* rpt;
+  const int32_t* col;
+  const double* val;
+  int32_t on_device; /* 1: the three pointers are device pointers on ctx's GPU */
+} spgemm_csr_view;
+
+/* SpgemmOptions (pipeline.hpp:78-91). */
+typedef struct spgemm_options {
+  char sym_preset[16];     /* "sym_1x" | "sym_1.2x" | "sym_1.5x"           */
+  char num_preset[16];     /* "num_1x" | "num_1.5x" | "num_2x" | "num_3x"  */
+  int32_t workers;         /* CPU pool size in the reference; reported only */
+  int32_t overlap;         /* stream-ordered C allocation overlap on/off    */
+  int32_t deterministic;   /* stable (1) or unordered (0) bin scatter       */
+  int64_t chunk_rows;      /* CPU task granularity in the reference; unused */
+  int64_t hash_scale;      /* HashParams::hash_scale, positive odd          */
+  int32_t has_sym_launch_order;
+  int32_t sym_launch_order[SPGEMM_NUM_BINS];
+  int32_t has_num_launch_order;
+  int32_t num_launch_order[SPGEMM_NUM_BINS];
+} spgemm_options;
+
+/* StepTimings (pipeline.hpp:93-102), seconds, measured with CUDA events. */
+typedef struct spgemm_timings {
+  double setup, sym_binning, symbolic, rpt_alloc, num_binning, numeric, cleanup, total;
+} spgemm_timings;
+
+/* SpgemmOutput minus the matrix (pipeline.hpp:104-110) + MatrixStats
+ * (reference.hpp:23-31) + AllocStats counters (pipeline.hpp:45-50). */
+typedef struct spgemm_report {
+  int64_t rows;
+  int64_t nnz;
+  double nnz_per_row_mean;
+  int64_t max_nnz_per_row;
+  int64_t total_nprod;
+  int64_t nnz_of_product;
+  double cr;
+  spgemm_timings timings;
+  int64_t spilled_rows;
+  int32_t workers;
+  int64_t metadata_calls, metadata_bytes, output_calls, output_bytes;
+} spgemm_report;
+
+/* BinConfig (binning.hpp:29-34). phase 0 symbolic, 1 numeric. */
+typedef struct spgemm_bin_config {
+  int32_t phase;
+  int64_t upper[SPGEMM_NUM_BINS];
+  int64_t table_size[SPGEMM_NUM_BINS];
+  char preset_name[16];
+} spgemm_bin_config;
+
+/* BinningResult scalars (binning.hpp:90-102). */
+typedef struct spgemm_binning_info {
+  int64_t bin_size[SPGEMM_NUM_BINS];
+  int64_t bin_offset[SPGEMM_NUM_BINS];
+  int64_t max_metric;
+  int64_t total_metric;
+  int32_t fast_path;
+} spgemm_binning_info;
+
+/* BinStrategy / ExecutionPlan (pipeline.hpp:21-39). tier 0 fixed, 1 heap. */
+typedef struct spgemm_bin_strategy {
+  int32_t bin;
+  int64_t metric_lo, metric_hi, table_size;
+  int32_t tier;
+  int64_t spill_threshold;
+  int32_t launch_rank;
+} spgemm_bin_strategy;
+
+typedef struct spgemm_plan {
+  int32_t phase;
+  spgemm_bin_config config;
+  spgemm_bin_strategy strategies[SPGEMM_NUM_BINS];
+  int32_t launch_order[SPGEMM_NUM_BINS];
+} spgemm_plan;
+
+/* ------------------------------------------------------------- context */
+spgemm_status spgemm_ctx_create(int32_t device, spgemm_ctx** out);
+void spgemm_ctx_destroy(spgemm_ctx* ctx);
+const char* spgemm_last_error(void);
+int32_t spgemm_ctx_device(const spgemm_ctx* ctx);
+int32_t spgemm_ctx_num_sms(const spgemm_ctx* ctx);
+/* Number of kernels this library launched on ctx since creation. */
+int64_t spgemm_ctx_kernel_launches(const spgemm_ctx* ctx);
+spgemm_status spgemm_ctx_synchronize(spgemm_ctx* ctx);
+/* The stream all pipeline work is ordered on (cudaStream_t as void*). */
+void* spgemm_ctx_stream(spgemm_ctx* ctx);
+
+/* Per-kernel device time: when profiling is on, every launch is bracketed by
+ * CUDA events on the stream it is launched on. The summary (aggregated by
+ * kernel name, then cleared) synchronises the device. */
+typedef struct spgemm_kernel_time {
+  char name[48];
+  int64_t launches;
+  double total_ms;
+} spgemm_kernel_time;
+void spgemm_ctx_set_profiling(spgemm_ctx* ctx, int32_t on);
+int32_t spgemm_ctx_profile_summary(spgemm_ctx* ctx, spgemm_kernel_time* out, int32_t max);
+
+/* ------------------------------------------------------- configuration */
+void spgemm_options_default(spgemm_options* opts);
+/* preset() (binning.cpp:33-66): INVALID_ARGUMENT for unknown names. */
+spgemm_status spgemm_preset(int32_t phase, const char* name, spgemm_bin_config* out);
+/* classify() (binning.cpp:75-82). */
+int32_t spgemm_classify(int64_t value, const spgemm_bin_config* config);
+/* make_execution_plan() (pipeline.cpp:64-87). */
+spgemm_status spgemm_make_plan(const spgemm_bin_config* config, spgemm_plan* out);
+
+/* --------------------------------------------------- SpgemmPipeline API */
+/* SpgemmPipeline ctor (pipeline.cpp:109-134): validates shapes/options and
+ * stages A and B in HBM (host views are copied, device views borrowed). */
+spgemm_status spgemm_pipeline_create(spgemm_ctx* ctx, const spgemm_csr_view* a,
+                                     const spgemm_csr_view* b, const spgemm_options* opts,
+                                     spgemm_pipeline** out);
+void spgemm_pipeline_destroy(spgemm_pipeline* p);
+spgemm_status spgemm_pipeline_setup(spgemm_pipeline* p);            /* pipeline.cpp:152-220 */
+spgemm_status spgemm_pipeline_symbolic_binning(spgemm_pipeline* p); /* pipeline.cpp:222-230 */
+spgemm_status spgemm_pipeline_run_symbolic(spgemm_pipeline* p);     /* pipeline.cpp:232-239 */
+spgemm_status spgemm_pipeline_numeric_binning(spgemm_pipeline* p);  /* pipeline.cpp:241-265 */
+spgemm_status spgemm_pipeline_finalize_rpt(spgemm_pipeline* p, int64_t* total); /* :278-294 */
+spgemm_status spgemm_pipeline_run_numeric(spgemm_pipeline* p);      /* pipeline.cpp:296-302 */
+spgemm_status spgemm_pipeline_finish(spgemm_pipeline* p, spgemm_report* report); /* :435-462 */
+spgemm_status spgemm_pipeline_run(spgemm_pipeline* p, spgemm_report* report);    /* :464-472 */
+/* rpt_region() (pipeline.cpp:148-150): copies the M-slot region to host. */
+spgemm_status spgemm_pipeline_rpt_region(spgemm_pipeline* p, int64_t* host_out);
+/* binning() accessor: scalars, and the bins array (int64, M) when non-NULL. */
+spgemm_status spgemm_pipeline_binning(spgemm_pipeline* p, spgemm_binning_info* info,
+                                      int64_t* bins_host);
+spgemm_status spgemm_pipeline_plan(spgemm_pipeline* p, int32_t phase, spgemm_plan* out);
+/* After finish(): hands C (device-resident) to the caller. */
+spgemm_status spgemm_pipeline_take_result(spgemm_pipeline* p, spgemm_matrix** c);
+
+/* multiply() (pipeline.hpp:170-173): one-shot C = A*B, C stays on device. */
+spgemm_status spgemm_multiply(spgemm_ctx* ctx, const spgemm_csr_view* a, const spgemm_csr_view* b,
+                              const spgemm_options* opts, spgemm_matrix** c,
+                              spgemm_report* report);
+
+/* ------------------------------------------------------ result matrices */
+void spgemm_matrix_shape(const spgemm_matrix* m, int64_t* rows, int64_t* cols, int64_t* nnz);
+void spgemm_matrix_device_ptrs(const spgemm_matrix* m, const int64_t** rpt, const int32_t** col,
+                               const double** val);
+/* D2H of C into caller buffers (rows+1, nnz, nnz entries). */
+spgemm_status spgemm_matrix_download(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t* rpt,
+                                     int32_t* col, double* val);
+void spgemm_matrix_free(spgemm_matrix* m);
+
+/* ----------------------------------------------- standalone GPU kernels */
+/* compute_nprod() (reference.cpp:37-55) on the device: out[M] host or device. */
+spgemm_status spgemm_compute_nprod(spgemm_ctx* ctx, const spgemm_csr_view* a,
+                                   const spgemm_csr_view* b, int64_t* out_host,
+                                   int64_t* total);
+/* build_rpt() / exclusive_sum_inplace() (pipeline.cpp:104-107, binning.cpp:117-168):
+ * in-place exclusive sum of n int64 host values on the GPU; returns total. */
+spgemm_status spgemm_build_rpt(spgemm_ctx* ctx, int64_t* values_host, int64_t n, int64_t* total);
+/* run_binning() (binning.cpp:281-313) on the device for a host metric. */
+spgemm_status spgemm_run_binning(spgemm_ctx* ctx, const int64_t* metric_host, int64_t m,
+                                 const spgemm_bin_config* config, int32_t deterministic,
+                                 int64_t* bins_host, spgemm_binning_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPGEMM_CAPI_H_ */

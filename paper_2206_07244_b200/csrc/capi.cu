@@ -1,0 +1,1236 @@
+// capi.cu -- host side of the B200-native OpSparse SpGEMM behind the C ABI in
+// include/spgemm_capi.h. One TU: the stage machine of SpgemmPipeline
+// (pipeline.cpp:109-472) re-designed around CUDA streams/events and
+// stream-ordered allocation, driving the sm_100a kernels in kernels.cuh.
+//
+// Differences by design (B200-first, not a port):
+//   * TaskPool/WaitGroup (task_pool.hpp) -> one stream per bin, launched in the
+//     plan's launch order (pipeline.cpp:84), joined with events.
+//   * MetadataArena (pipeline.cpp:89-102) -> one cudaMallocAsync arena holding
+//     int32 bins, per-row-block counts, scan state, spill ids and phase info.
+//   * allocate_output on std::async (pipeline.cpp:254-257) -> cudaMallocAsync
+//     of C.col/C.val on a side stream while the numeric scatter runs.
+//   * StepTimings from CUDA events recorded at the step boundaries.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <new>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "kernels.cuh"
+#include "spgemm_capi.h"
+
+using namespace spgemm_b200;
+
+// ------------------------------------------------------------------ errors
+namespace {
+
+thread_local std::string g_err;
+
+struct Err {
+  spgemm_status s;
+  std::string m;
+};
+
+[[noreturn]] void fail(spgemm_status s, std::string m) { throw Err{s, std::move(m)}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? SPGEMM_OUT_OF_MEMORY : SPGEMM_CUDA_ERROR,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+spgemm_status guard(F&& f) {
+  try {
+    f();
+    return SPGEMM_OK;
+  } catch (const Err& e) {
+    g_err = e.m;
+    return e.s;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SPGEMM_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SPGEMM_LOGIC_ERROR;
+  }
+}
+
+// -------------------------------------------------------------- presets
+// binning.cpp:26-66 -- the same published ranges and capacities.
+constexpr int64_t kNoUpper = std::numeric_limits<int64_t>::max();
+constexpr int64_t kSymTable[kNumBins] = {32, 512, 1024, 2048, 4096, 8192, 12287, 24575};
+constexpr int64_t kNumTable[kNumBins] = {31, 255, 511, 1023, 2047, 4095, 8191, 0};
+
+struct PresetRow {
+  const char* name;
+  int phase;
+  int64_t upper[kNumBins];
+};
+constexpr PresetRow kPresets[] = {
+    {"sym_1x", 0, {32, 512, 1024, 2048, 4096, 8192, 12287, kNoUpper}},
+    {"sym_1.2x", 0, {26, 426, 853, 1706, 3413, 6826, 10240, kNoUpper}},
+    {"sym_1.5x", 0, {21, 341, 682, 1365, 2730, 5461, 8191, kNoUpper}},
+    {"num_1x", 1, {31, 255, 511, 1023, 2047, 4095, 8191, kNoUpper}},
+    {"num_1.5x", 1, {21, 192, 384, 768, 1536, 3072, 5460, kNoUpper}},
+    {"num_2x", 1, {16, 128, 256, 512, 1024, 2048, 4096, kNoUpper}},
+    {"num_3x", 1, {10, 85, 170, 341, 682, 1365, 2730, kNoUpper}},
+};
+
+bool find_preset(int phase, const char* name, spgemm_bin_config* out) {
+  for (const PresetRow& r : kPresets) {
+    if (r.phase == phase && std::strcmp(r.name, name) == 0) {
+      out->phase = phase;
+      for (int j = 0; j < kNumBins; ++j) {
+        out->upper[j] = r.upper[j];
+        out->table_size[j] = phase == 0 ? kSymTable[j] : kNumTable[j];
+      }
+      std::memset(out->preset_name, 0, sizeof(out->preset_name));
+      std::strncpy(out->preset_name, r.name, sizeof(out->preset_name) - 1);
+      return true;
+    }
+  }
+  return false;
+}
+
+int classify_host(int64_t v, const spgemm_bin_config& c) {
+  for (int j = 0; j < kNumBins - 1; ++j)
+    if (v <= c.upper[j]) return j;
+  return kNumBins - 1;
+}
+
+// pipeline.cpp:64-87
+void make_plan(const spgemm_bin_config& c, spgemm_plan* plan) {
+  std::memset(plan, 0, sizeof(*plan));
+  plan->phase = c.phase;
+  plan->config = c;
+  int64_t lo = 0;
+  for (int j = 0; j < kNumBins; ++j) {
+    spgemm_bin_strategy& s = plan->strategies[j];
+    s.bin = j;
+    s.metric_lo = lo;
+    s.metric_hi = c.upper[j];
+    if (s.metric_hi != kNoUpper) lo = s.metric_hi + 1;
+    s.table_size = c.table_size[j];
+    s.tier = s.table_size > 0 ? 0 : 1;
+    s.spill_threshold =
+        (c.phase == 0 && j == kNumBins - 1 && s.table_size > 0) ? s.table_size * 4 / 5 : 0;
+    s.launch_rank = kNumBins - 1 - j;
+  }
+  for (int j = 0; j < kNumBins; ++j) plan->launch_order[j] = j;
+  std::stable_sort(plan->launch_order, plan->launch_order + kNumBins, [&](int x, int y) {
+    return plan->strategies[x].launch_rank < plan->strategies[y].launch_rank;
+  });
+}
+
+void apply_launch_order(spgemm_plan* plan, const int32_t* order) {
+  int32_t sorted[kNumBins];
+  std::memcpy(sorted, order, sizeof(sorted));
+  std::sort(sorted, sorted + kNumBins);
+  for (int j = 0; j < kNumBins; ++j)
+    if (sorted[j] != j)
+      fail(SPGEMM_INVALID_ARGUMENT, "launch order must be a permutation of the bin indices");
+  for (int j = 0; j < kNumBins; ++j) plan->strategies[order[j]].launch_rank = j;
+  for (int j = 0; j < kNumBins; ++j) plan->launch_order[j] = j;
+  std::stable_sort(plan->launch_order, plan->launch_order + kNumBins, [&](int x, int y) {
+    return plan->strategies[x].launch_rank < plan->strategies[y].launch_rank;
+  });
+}
+
+BinUpper to_upper(const spgemm_bin_config& c) {
+  BinUpper u;
+  for (int j = 0; j < kNumBins; ++j) u.u[j] = c.upper[j];
+  return u;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+// ----------------------------------------------------------------- context
+struct spgemm_ctx {
+  int device = 0;
+  int num_sms = 0;
+  int max_smem = 0;
+  cudaStream_t main_s = nullptr, side_s = nullptr;
+  cudaStream_t bin_s[kNumBins] = {};
+  cudaEvent_t ev_fork = nullptr, ev_side = nullptr, ev_info = nullptr;
+  cudaEvent_t ev_join[kNumBins] = {};
+  DevInfo* h_info = nullptr;  // pinned, two slots
+  std::atomic<int64_t> launches{0};
+  std::mutex attr_mu;
+  std::unordered_set<const void*> attr_done;
+  // Optional per-kernel timing: events bracket every launch on its own stream.
+  bool prof = false;
+  struct ProfRec {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename Kern>
+void prepare_kernel(spgemm_ctx* ctx, Kern kern, size_t smem) {
+  const void* key = reinterpret_cast<const void*>(kern);
+  std::lock_guard<std::mutex> lock(ctx->attr_mu);
+  if (ctx->attr_done.count(key)) return;
+  ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(std::max<size_t>(smem, 48 * 1024))),
+     "cudaFuncSetAttribute");
+  ctx->attr_done.insert(key);
+}
+
+// Persistent grid: enough blocks to cover the work, at most one full wave of
+// resident blocks (148 SMs x occupancy).
+template <typename Kern>
+int persistent_grid(spgemm_ctx* ctx, Kern kern, int threads, size_t smem, int64_t work) {
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
+     "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (per_sm < 1) fail(SPGEMM_CUDA_ERROR, "kernel cannot be resident (shared memory too large)");
+  const int64_t cap = static_cast<int64_t>(per_sm) * ctx->num_sms;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(work, cap)));
+}
+
+void count_launch(spgemm_ctx* ctx, const char* what) {
+  ck(cudaGetLastError(), what);
+  ctx->launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+cudaEvent_t pooled_event(spgemm_ctx* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+// Brackets one kernel launch: counts it and, when profiling, records events
+// on the launching stream around it.
+struct LaunchScope {
+  spgemm_ctx* ctx;
+  std::string name;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  LaunchScope(spgemm_ctx* c, std::string n, cudaStream_t st) : ctx(c), name(std::move(n)), s(st) {
+    if (ctx->prof) {
+      a = pooled_event(ctx);
+      ck(cudaEventRecord(a, s), "prof event");
+    }
+  }
+  void done() {
+    count_launch(ctx, name.c_str());
+    if (a) {
+      cudaEvent_t b = pooled_event(ctx);
+      ck(cudaEventRecord(b, s), "prof event");
+      ctx->prof_recs.push_back({name, a, b});
+    }
+  }
+};
+
+#define SPG_LAUNCH(CTX, NAME, STREAM, ...)       \
+  do {                                           \
+    LaunchScope ls_((CTX), (NAME), (STREAM));    \
+    __VA_ARGS__;                                 \
+    ls_.done();                                  \
+  } while (0)
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  ck(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+  return p;
+}
+
+void dev_free(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+}  // namespace
+
+// -------------------------------------------------------- result matrices
+struct spgemm_matrix {
+  spgemm_ctx* ctx = nullptr;
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int64_t* rpt = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+};
+
+// ----------------------------------------------------------------- pipeline
+struct spgemm_pipeline {
+  enum Stage { kNew, kSetup, kSymBinned, kSymbolic, kNumBinned, kRptDone, kNumeric, kDone };
+
+  spgemm_ctx* ctx = nullptr;
+  spgemm_options opts{};
+  spgemm_plan sym_plan{}, num_plan{};
+  BinUpper sym_up{}, num_up{};
+  DevCsr A{}, B{};
+  int64_t a_nnz = 0, b_nnz = 0;
+  void* owned[6] = {};
+  int64_t M = 0;
+  int64_t nrb = 0, ntiles = 0;
+  uint32_t scale = 107;
+  double avg_b_len = 0;
+
+  int64_t* d_rpt = nullptr;
+  unsigned char* d_arena = nullptr;
+  size_t arena_bytes = 0;
+  int32_t* d_bins = nullptr;
+  int32_t* d_spill = nullptr;
+  int32_t* d_blk = nullptr;
+  int* d_flags = nullptr;
+  long long* d_sums = nullptr;
+  DevInfo* d_info_sym = nullptr;
+  DevInfo* d_info_num = nullptr;
+  int32_t* d_ccol = nullptr;
+  double* d_cval = nullptr;
+  bool alloc_pending = false;
+
+  DevInfo h_sym{}, h_num{};
+  spgemm_binning_info bin_info{};
+  int64_t total_nprod = 0, total_nnz = 0;
+  int stage = kNew;
+  cudaEvent_t ev[12] = {};
+  int64_t metadata_calls = 0, metadata_bytes = 0, output_calls = 0, output_bytes = 0;
+  double cleanup_s = 0;
+  bool result_taken = false;
+
+  void expect(int s, const char* op) {
+    if (stage != s)
+      fail(SPGEMM_LOGIC_ERROR, std::string("spgemm pipeline: ") + op + " called out of order");
+  }
+  void mark(int i) { ck(cudaEventRecord(ev[i], ctx->main_s), "cudaEventRecord"); }
+  double span(int i, int j) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, ev[i], ev[j]), "cudaEventElapsedTime");
+    return ms * 1e-3;
+  }
+  void fetch_info(DevInfo* d, DevInfo* h) {
+    ck(cudaMemcpyAsync(ctx->h_info, d, sizeof(DevInfo), cudaMemcpyDeviceToHost, ctx->main_s),
+       "D2H info");
+    ck(cudaStreamSynchronize(ctx->main_s), "cudaStreamSynchronize");
+    *h = *ctx->h_info;
+  }
+
+  void setup();
+  void symbolic_binning();
+  void run_symbolic();
+  void numeric_binning();
+  int64_t finalize_rpt();
+  void run_numeric();
+  void finish(spgemm_report* r);
+  void allocate_output(cudaStream_t s);
+  void launch_sym_bin(int bin, const RowList& rl, cudaStream_t s);
+  void launch_num_bin(int bin, const RowList& rl, cudaStream_t s, int32_t* gkeys, double* gvals,
+                      uint32_t* gbits, int64_t gslots, int64_t gwords, int gblocks);
+  void release(bool keep_result);
+};
+
+namespace {
+
+void stage_input(spgemm_ctx* ctx, const spgemm_csr_view* v, DevCsr* d, void** owned, int64_t* nnz) {
+  d->rows = v->rows;
+  d->cols = v->cols;
+  if (v->rows < 0 || v->cols < 0) fail(SPGEMM_INVALID_ARGUMENT, "negative matrix shape");
+  if (v->cols > std::numeric_limits<int32_t>::max())
+    fail(SPGEMM_INVALID_ARGUMENT, "column count exceeds the 32-bit index range");
+  if (v->rows >= std::numeric_limits<int32_t>::max())
+    fail(SPGEMM_INVALID_ARGUMENT, "row count exceeds the 32-bit row-id range");
+  if (!v->rpt) fail(SPGEMM_INVALID_ARGUMENT, "null rpt");
+  if (v->on_device) {
+    ck(cudaMemcpy(nnz, v->rpt + v->rows, sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H nnz");
+    d->rpt = v->rpt;
+    d->col = v->col;
+    d->val = v->val;
+    return;
+  }
+  *nnz = v->rpt[v->rows];
+  const size_t rb = static_cast<size_t>(v->rows + 1) * sizeof(int64_t);
+  const size_t cb = static_cast<size_t>(*nnz) * sizeof(int32_t);
+  const size_t vb = static_cast<size_t>(*nnz) * sizeof(double);
+  owned[0] = dev_alloc(rb, ctx->main_s);
+  owned[1] = dev_alloc(cb, ctx->main_s);
+  owned[2] = dev_alloc(vb, ctx->main_s);
+  ck(cudaMemcpyAsync(owned[0], v->rpt, rb, cudaMemcpyHostToDevice, ctx->main_s), "H2D rpt");
+  if (cb) ck(cudaMemcpyAsync(owned[1], v->col, cb, cudaMemcpyHostToDevice, ctx->main_s), "H2D col");
+  if (vb) ck(cudaMemcpyAsync(owned[2], v->val, vb, cudaMemcpyHostToDevice, ctx->main_s), "H2D val");
+  d->rpt = static_cast<const int64_t*>(owned[0]);
+  d->col = static_cast<const int32_t*>(owned[1]);
+  d->val = static_cast<const double*>(owned[2]);
+}
+
+}  // namespace
+
+void spgemm_pipeline::setup() {
+  expect(kNew, "setup");
+  mark(0);
+  cudaStream_t s = ctx->main_s;
+  nrb = ceil_div(M, kRowsPerBlock);
+  ntiles = ceil_div(M + 1, kScanTile);
+  d_rpt = static_cast<int64_t*>(dev_alloc(static_cast<size_t>(M + 1) * 8, s));
+  metadata_calls += 1;
+  metadata_bytes += (M + 1) * 8;
+  // One arena for all binning metadata, sized from the row count alone.
+  size_t off = 0;
+  const size_t o_info = off;
+  off = align_up(off + 2 * sizeof(DevInfo), 256);
+  const size_t o_blk = off;
+  off = align_up(off + static_cast<size_t>(std::max<int64_t>(nrb, 1)) * kNumBins * 4, 256);
+  const size_t o_flags = off;
+  off = align_up(off + static_cast<size_t>(ntiles) * 4, 256);
+  const size_t o_sums = off;
+  off = align_up(off + static_cast<size_t>(ntiles) * 16, 256);
+  const size_t o_bins = off;
+  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 4, 256);
+  const size_t o_spill = off;
+  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 4, 256);
+  arena_bytes = off;
+  d_arena = static_cast<unsigned char*>(dev_alloc(arena_bytes, s));
+  metadata_calls += 1;
+  metadata_bytes += static_cast<int64_t>(arena_bytes);
+  d_info_sym = reinterpret_cast<DevInfo*>(d_arena + o_info);
+  d_info_num = d_info_sym + 1;
+  d_blk = reinterpret_cast<int32_t*>(d_arena + o_blk);
+  d_flags = reinterpret_cast<int*>(d_arena + o_flags);
+  d_sums = reinterpret_cast<long long*>(d_arena + o_sums);
+  d_bins = reinterpret_cast<int32_t*>(d_arena + o_bins);
+  d_spill = reinterpret_cast<int32_t*>(d_arena + o_spill);
+  ck(cudaMemsetAsync(d_info_sym, 0, 2 * sizeof(DevInfo), s), "memset info");
+  if (M > 0) {
+    SPG_LAUNCH(ctx, "k_setup_nprod", s,
+               k_setup_nprod<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(A, B.rpt, d_rpt, M, sym_up,
+                                                                      d_blk, d_info_sym));
+  } else {
+    ck(cudaMemsetAsync(d_rpt, 0, 8, s), "memset rpt");
+  }
+  fetch_info(d_info_sym, &h_sym);
+  if (h_sym.total > static_cast<unsigned long long>(std::numeric_limits<int64_t>::max()))
+    fail(SPGEMM_OVERFLOW, "spgemm: intermediate-product count overflowed 64 bits");
+  total_nprod = static_cast<int64_t>(h_sym.total);
+  mark(1);
+  stage = kSetup;
+}
+
+void spgemm_pipeline::symbolic_binning() {
+  expect(kSetup, "symbolic_binning");
+  mark(2);
+  cudaStream_t s = ctx->main_s;
+  std::memset(&bin_info, 0, sizeof(bin_info));
+  bin_info.max_metric = h_sym.max_metric;
+  bin_info.total_metric = static_cast<int64_t>(h_sym.total);
+  const bool fast = M == 0 || h_sym.max_metric <= sym_up.u[0];
+  if (fast) {
+    bin_info.fast_path = 1;
+    bin_info.bin_size[0] = M;
+  } else {
+    SPG_LAUNCH(ctx, "k_bin_offsets", s,
+               k_bin_offsets<<<1, 1024, 0, s>>>(d_blk, nrb, M, sym_up.u[0], d_info_sym));
+    SPG_LAUNCH(ctx, "k_bin_scatter", s,
+               k_bin_scatter<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(d_rpt, M, sym_up, d_blk,
+                                                                      d_bins, d_info_sym));
+    DevInfo tmp;
+    fetch_info(d_info_sym, &tmp);
+    h_sym.spill_count = tmp.spill_count;
+    for (int j = 0; j < kNumBins; ++j) {
+      bin_info.bin_size[j] = tmp.bin_size[j];
+      bin_info.bin_offset[j] = tmp.bin_offset[j];
+    }
+  }
+  mark(3);
+  stage = kSymBinned;
+}
+
+// ------------------------------------------------------- symbolic dispatch
+// Tier choice per bin from the preset's inclusive upper bound on nprod (the
+// bin invariant guarantees the table never fills). G (lanes per row) follows
+// the mean B row length so the lanes striding a B row stay busy.
+void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s) {
+  const int64_t u = sym_plan.config.upper[bin];
+  const bool g8 = avg_b_len <= 8.0;
+  auto group = [&](auto kern, int G, int T, int NGRP) {
+    const size_t smem = static_cast<size_t>(NGRP) * T * 4;
+    prepare_kernel(ctx, kern, smem);
+    const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
+    SPG_LAUNCH(ctx, "k_sym_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
+               kern<<<grid, G * NGRP, smem, s>>>(rl, A, B, d_rpt, scale));
+  };
+  auto block = [&](auto kern, int T, int threads) {
+    const size_t smem = static_cast<size_t>(T) * 4;
+    prepare_kernel(ctx, kern, smem);
+    const int grid = persistent_grid(ctx, kern, threads, smem, rl.count);
+    SPG_LAUNCH(ctx, "k_sym_block<" + std::to_string(T) + ">", s,
+               kern<<<grid, threads, smem, s>>>(rl, A, B, d_rpt, scale, d_spill, d_info_sym,
+                                     static_cast<int>(sym_plan.strategies[bin].spill_threshold)));
+  };
+  if (bin == kNumBins - 1) {
+    block(k_sym_block<32768, 1024, true>, 32768, 1024);
+    // Heap-tier recompute of the spilled rows (pipeline.cpp:315-348): a pool
+    // of per-block global tables; the kernel reads the spill count on device.
+    long long want = 2 * std::min<long long>(h_sym.max_metric, B.cols);
+    int64_t slots = 2;
+    while (slots < want) slots <<= 1;
+    const int64_t budget = int64_t(4) << 30;
+    const int blocks = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({2LL * ctx->num_sms, rl.count, budget / (slots * 4)})));
+    int32_t* pool = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(slots) * 4 * blocks, s));
+    SPG_LAUNCH(ctx, "k_sym_spill", s,
+               k_sym_spill<<<blocks, 1024, 0, s>>>(A, B, d_rpt, d_spill, d_info_sym, pool, slots, scale));
+    dev_free(pool, s);
+    return;
+  }
+  if (u <= 32) {
+    if (g8) group(k_sym_group<8, 64, 32>, 8, 64, 32);
+    else group(k_sym_group<32, 64, 8>, 32, 64, 8);
+  } else if (u <= 512) {
+    if (g8) group(k_sym_group<8, 1024, 16>, 8, 1024, 16);
+    else group(k_sym_group<32, 1024, 8>, 32, 1024, 8);
+  } else if (u <= 1024) {
+    if (g8) group(k_sym_group<8, 2048, 8>, 8, 2048, 8);
+    else group(k_sym_group<32, 2048, 8>, 32, 2048, 8);
+  } else if (u <= 2048) {
+    block(k_sym_block<4096, 256, false>, 4096, 256);
+  } else if (u <= 4096) {
+    block(k_sym_block<8192, 256, false>, 8192, 256);
+  } else {
+    block(k_sym_block<16384, 512, false>, 16384, 512);
+  }
+}
+
+void spgemm_pipeline::run_symbolic() {
+  expect(kSymBinned, "run_symbolic");
+  mark(4);
+  ck(cudaEventRecord(ctx->ev_fork, ctx->main_s), "ev_fork");
+  for (int r = 0; r < kNumBins; ++r) {
+    const int bin = sym_plan.launch_order[r];
+    if (bin_info.bin_size[bin] == 0) continue;
+    cudaStream_t s = ctx->bin_s[bin];
+    ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
+    RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path};
+    launch_sym_bin(bin, rl, s);
+    ck(cudaEventRecord(ctx->ev_join[bin], s), "ev_join");
+    ck(cudaStreamWaitEvent(ctx->main_s, ctx->ev_join[bin], 0), "wait join");
+  }
+  mark(5);
+  stage = kSymbolic;
+}
+
+void spgemm_pipeline::allocate_output(cudaStream_t s) {
+  d_ccol = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(total_nnz) * 4, s));
+  d_cval = static_cast<double*>(dev_alloc(static_cast<size_t>(total_nnz) * 8, s));
+  output_calls += 2;
+  output_bytes += total_nnz * 12;
+}
+
+void spgemm_pipeline::numeric_binning() {
+  expect(kSymbolic, "numeric_binning");
+  mark(6);
+  cudaStream_t s = ctx->main_s;
+  std::memset(&bin_info, 0, sizeof(bin_info));
+  if (M > 0) {
+    SPG_LAUNCH(ctx, "k_pass1", s,
+               k_pass1<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(d_rpt, M, num_up, d_blk, d_info_num));
+    SPG_LAUNCH(ctx, "k_bin_offsets", s,
+               k_bin_offsets<<<1, 1024, 0, s>>>(d_blk, nrb, M, num_up.u[0], d_info_num));
+  }
+  // The pass-1 total sizes C; read it back while the scatter runs and start
+  // the C allocation on the side lane (pipeline.cpp:245-257).
+  ck(cudaMemcpyAsync(ctx->h_info + 1, d_info_num, sizeof(DevInfo), cudaMemcpyDeviceToHost, s),
+     "D2H num info");
+  ck(cudaEventRecord(ctx->ev_info, s), "ev_info");
+  if (M > 0) {
+    SPG_LAUNCH(ctx, "k_bin_scatter", s,
+               k_bin_scatter<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(d_rpt, M, num_up, d_blk,
+                                                                      d_bins, d_info_num));
+  }
+  ck(cudaEventSynchronize(ctx->ev_info), "sync num info");
+  h_num = ctx->h_info[1];
+  if (M == 0) h_num.fast_path = 1;
+  if (h_num.total > static_cast<unsigned long long>(std::numeric_limits<int64_t>::max()))
+    fail(SPGEMM_OVERFLOW, "spgemm: nonzero count overflowed 64 bits");
+  total_nnz = static_cast<int64_t>(h_num.total);
+  if (opts.overlap) {
+    ck(cudaStreamWaitEvent(ctx->side_s, ctx->ev_info, 0), "side wait");
+    allocate_output(ctx->side_s);
+    ck(cudaEventRecord(ctx->ev_side, ctx->side_s), "ev_side");
+    alloc_pending = true;
+  }
+  bin_info.max_metric = h_num.max_metric;
+  bin_info.total_metric = total_nnz;
+  bin_info.fast_path = h_num.fast_path;
+  for (int j = 0; j < kNumBins; ++j) {
+    bin_info.bin_size[j] = h_num.bin_size[j];
+    bin_info.bin_offset[j] = h_num.bin_offset[j];
+  }
+  mark(7);
+  stage = kNumBinned;
+}
+
+int64_t spgemm_pipeline::finalize_rpt() {
+  expect(kNumBinned, "finalize_rpt");
+  mark(8);
+  cudaStream_t s = ctx->main_s;
+  ck(cudaMemsetAsync(d_flags, 0, static_cast<size_t>(ntiles) * 4, s), "memset flags");
+  SPG_LAUNCH(ctx, "k_scan", s,
+             k_scan<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(d_rpt, M + 1, d_flags, d_sums,
+                                                                 d_sums + ntiles, d_info_num));
+  DevInfo tmp;
+  fetch_info(d_info_num, &tmp);
+  if (tmp.scan_total != total_nnz)
+    fail(SPGEMM_LOGIC_ERROR, "spgemm: exclusive sum disagrees with binning total");
+  if (alloc_pending) {
+    ck(cudaStreamWaitEvent(s, ctx->ev_side, 0), "join alloc lane");
+    alloc_pending = false;
+  } else {
+    allocate_output(s);
+  }
+  mark(9);
+  stage = kRptDone;
+  return total_nnz;
+}
+
+// -------------------------------------------------------- numeric dispatch
+void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s, int32_t* gkeys,
+                                     double* gvals, uint32_t* gbits, int64_t gslots,
+                                     int64_t gwords, int gblocks) {
+  const int64_t u = num_plan.config.upper[bin];
+  const bool g8 = avg_b_len <= 8.0;
+  auto group = [&](auto kern, int G, int T, int E, int NGRP) {
+    const size_t smem = static_cast<size_t>(NGRP) * (T * 12 + G * E * 8);
+    prepare_kernel(ctx, kern, smem);
+    const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
+    SPG_LAUNCH(ctx, "k_num_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
+               kern<<<grid, G * NGRP, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
+  };
+  auto block = [&](auto kern, int T, int threads, int nmax) {
+    const size_t smem = static_cast<size_t>(T) * 12 + static_cast<size_t>(nmax) * 8;
+    prepare_kernel(ctx, kern, smem);
+    const int grid = persistent_grid(ctx, kern, threads, smem, rl.count);
+    SPG_LAUNCH(ctx, "k_num_block<" + std::to_string(T) + ">", s,
+               kern<<<grid, threads, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
+  };
+  if (bin == kNumBins - 1 || u > 4096) {
+    SPG_LAUNCH(ctx, "k_num_global", s,
+               k_num_global<<<gblocks, kGlobalThreads, 0, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, gkeys,
+                                                    gvals, gbits, gslots, gwords, d_info_num));
+  } else if (u <= 32) {
+    if (g8) group(k_num_group<8, 64, 4, 32>, 8, 64, 4, 32);
+    else group(k_num_group<32, 64, 1, 8>, 32, 64, 1, 8);
+  } else if (u <= 128) {
+    if (g8) group(k_num_group<8, 256, 16, 16>, 8, 256, 16, 16);
+    else group(k_num_group<32, 256, 4, 8>, 32, 256, 4, 8);
+  } else if (u <= 256) {
+    group(k_num_group<32, 512, 8, 8>, 32, 512, 8, 8);
+  } else if (u <= 512) {
+    group(k_num_group<32, 1024, 16, 4>, 32, 1024, 16, 4);
+  } else if (u <= 1024) {
+    block(k_num_block<2048, 256, 1024>, 2048, 256, 1024);
+  } else if (u <= 2048) {
+    block(k_num_block<4096, 256, 2048>, 4096, 256, 2048);
+  } else {
+    block(k_num_block<8192, 512, 4096>, 8192, 512, 4096);
+  }
+}
+
+void spgemm_pipeline::run_numeric() {
+  expect(kRptDone, "run_numeric");
+  mark(10);
+  // Global (heap) tier pool, sized from the exact max row nnz of pass 1.
+  int64_t grows = 0;
+  for (int j = 0; j < kNumBins; ++j)
+    if (j == kNumBins - 1 || num_plan.config.upper[j] > 4096) grows += bin_info.bin_size[j];
+  int32_t* gkeys = nullptr;
+  double* gvals = nullptr;
+  uint32_t* gbits = nullptr;
+  int64_t gslots = 0, gwords = 0;
+  int gblocks = 0;
+  if (grows > 0) {
+    gslots = 2;
+    while (gslots < 2 * h_num.max_metric) gslots <<= 1;
+    gwords = std::min<int64_t>(int64_t(1) << 17, std::max<int64_t>(1, ceil_div(B.cols, 32)));
+    const int64_t per_block = gslots * 12 + gwords * 8;
+    const int64_t budget = int64_t(8) << 30;
+    gblocks = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({2LL * ctx->num_sms, grows, budget / per_block})));
+    gkeys = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(gslots) * 4 * gblocks, ctx->main_s));
+    gvals = static_cast<double*>(dev_alloc(static_cast<size_t>(gslots) * 8 * gblocks, ctx->main_s));
+    gbits = static_cast<uint32_t*>(dev_alloc(static_cast<size_t>(gwords) * 8 * gblocks, ctx->main_s));
+  }
+  ck(cudaEventRecord(ctx->ev_fork, ctx->main_s), "ev_fork");
+  for (int r = 0; r < kNumBins; ++r) {
+    const int bin = num_plan.launch_order[r];
+    if (bin_info.bin_size[bin] == 0) continue;
+    cudaStream_t s = ctx->bin_s[bin];
+    ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
+    RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path};
+    launch_num_bin(bin, rl, s, gkeys, gvals, gbits, gslots, gwords, gblocks);
+    ck(cudaEventRecord(ctx->ev_join[bin], s), "ev_join");
+    ck(cudaStreamWaitEvent(ctx->main_s, ctx->ev_join[bin], 0), "wait join");
+  }
+  dev_free(gkeys, ctx->main_s);
+  dev_free(gvals, ctx->main_s);
+  dev_free(gbits, ctx->main_s);
+  mark(11);
+  stage = kNumeric;
+}
+
+void spgemm_pipeline::finish(spgemm_report* r) {
+  expect(kNumeric, "finish");
+  DevInfo sym, num;
+  fetch_info(d_info_sym, &sym);
+  fetch_info(d_info_num, &num);
+  if (num.error & kErrNumericCount)
+    fail(SPGEMM_LOGIC_ERROR, "spgemm: numeric row nnz disagrees with symbolic result");
+  spgemm_report rep;
+  std::memset(&rep, 0, sizeof(rep));
+  rep.rows = M;
+  rep.nnz = a_nnz;
+  rep.nnz_per_row_mean = M > 0 ? static_cast<double>(a_nnz) / static_cast<double>(M) : 0.0;
+  rep.max_nnz_per_row = sym.a_max_row;
+  rep.total_nprod = total_nprod;
+  rep.nnz_of_product = total_nnz;
+  rep.cr = total_nnz > 0 ? static_cast<double>(total_nprod) / static_cast<double>(total_nnz) : 0.0;
+  rep.spilled_rows = static_cast<int64_t>(sym.spill_count);
+  rep.workers = opts.workers > 0 ? opts.workers : ctx->num_sms;
+  rep.timings.setup = span(0, 1);
+  rep.timings.sym_binning = span(2, 3);
+  rep.timings.symbolic = span(4, 5);
+  rep.timings.num_binning = span(6, 7);
+  rep.timings.rpt_alloc = span(8, 9);
+  rep.timings.numeric = span(10, 11);
+  // Cleanup: the metadata arena goes only now, after every kernel of both
+  // phases (pipeline.cpp:449-455).
+  const auto t0 = std::chrono::steady_clock::now();
+  dev_free(d_arena, ctx->main_s);
+  d_arena = nullptr;
+  rep.timings.cleanup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  rep.timings.total = rep.timings.setup + rep.timings.sym_binning + rep.timings.symbolic +
+                      rep.timings.rpt_alloc + rep.timings.num_binning + rep.timings.numeric +
+                      rep.timings.cleanup;
+  rep.metadata_calls = metadata_calls;
+  rep.metadata_bytes = metadata_bytes;
+  rep.output_calls = output_calls;
+  rep.output_bytes = output_bytes;
+  if (r) *r = rep;
+  stage = kDone;
+}
+
+void spgemm_pipeline::release(bool keep_result) {
+  cudaStream_t s = ctx->main_s;
+  if (alloc_pending) {
+    cudaStreamWaitEvent(s, ctx->ev_side, 0);
+    alloc_pending = false;
+  }
+  for (void*& p : owned) {
+    dev_free(p, s);
+    p = nullptr;
+  }
+  dev_free(d_arena, s);
+  d_arena = nullptr;
+  if (!keep_result) {
+    dev_free(d_rpt, s);
+    dev_free(d_ccol, s);
+    dev_free(d_cval, s);
+  }
+  d_rpt = nullptr;
+  d_ccol = nullptr;
+  d_cval = nullptr;
+}
+
+// ================================================================= C ABI
+extern "C" {
+
+const char* spgemm_last_error(void) { return g_err.c_str(); }
+
+void spgemm_options_default(spgemm_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  std::strncpy(o->sym_preset, "sym_1.2x", sizeof(o->sym_preset) - 1);
+  std::strncpy(o->num_preset, "num_2x", sizeof(o->num_preset) - 1);
+  o->workers = 0;
+  o->overlap = 1;
+  o->deterministic = 1;
+  o->chunk_rows = 4096;
+  o->hash_scale = 107;
+}
+
+spgemm_status spgemm_ctx_create(int32_t device, spgemm_ctx** out) {
+  *out = nullptr;
+  return guard([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail(SPGEMM_NO_DEVICE, "no CUDA device visible");
+    }
+    if (device < 0 || device >= n) fail(SPGEMM_INVALID_ARGUMENT, "device index out of range");
+    auto* c = new spgemm_ctx();
+    c->device = device;
+    try {
+      DeviceGuard g(device);
+      cudaDeviceProp prop;
+      ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+      if (prop.major < 10)
+        fail(SPGEMM_NO_DEVICE, "this build targets sm_100a (B200); device is sm_" +
+                                   std::to_string(prop.major) + std::to_string(prop.minor));
+      c->num_sms = prop.multiProcessorCount;
+      c->max_smem = static_cast<int>(prop.sharedMemPerBlockOptin);
+      ck(cudaStreamCreateWithFlags(&c->main_s, cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithFlags(&c->side_s, cudaStreamNonBlocking), "stream");
+      for (auto& s : c->bin_s) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&c->ev_info, cudaEventDisableTiming), "event");
+      for (auto& e : c->ev_join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ck(cudaMallocHost(&c->h_info, 2 * sizeof(DevInfo)), "cudaMallocHost");
+      // Keep freed blocks in the stream-ordered pool: repeated multiplies
+      // reuse HBM without returning it to the driver.
+      cudaMemPool_t pool;
+      ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+      uint64_t thresh = std::numeric_limits<uint64_t>::max();
+      ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh), "pool attr");
+    } catch (...) {
+      spgemm_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void spgemm_ctx_destroy(spgemm_ctx* c) {
+  if (!c) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  if (c->main_s) cudaStreamSynchronize(c->main_s);
+  for (auto& s : c->bin_s)
+    if (s) cudaStreamDestroy(s);
+  if (c->side_s) cudaStreamDestroy(c->side_s);
+  if (c->main_s) cudaStreamDestroy(c->main_s);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_side) cudaEventDestroy(c->ev_side);
+  if (c->ev_info) cudaEventDestroy(c->ev_info);
+  for (auto& e : c->ev_join)
+    if (e) cudaEventDestroy(e);
+  for (auto& r : c->prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto& e : c->ev_pool) cudaEventDestroy(e);
+  if (c->h_info) cudaFreeHost(c->h_info);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete c;
+}
+
+int32_t spgemm_ctx_device(const spgemm_ctx* c) { return c->device; }
+int32_t spgemm_ctx_num_sms(const spgemm_ctx* c) { return c->num_sms; }
+int64_t spgemm_ctx_kernel_launches(const spgemm_ctx* c) { return c->launches.load(); }
+
+void spgemm_ctx_set_profiling(spgemm_ctx* c, int32_t on) { c->prof = on != 0; }
+
+int32_t spgemm_ctx_profile_summary(spgemm_ctx* c, spgemm_kernel_time* out, int32_t max) {
+  int32_t n = 0;
+  guard([&] {
+    DeviceGuard g(c->device);
+    ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    std::vector<spgemm_kernel_time> agg;
+    for (auto& r : c->prof_recs) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+      auto it = std::find_if(agg.begin(), agg.end(), [&](const spgemm_kernel_time& k) {
+        return r.name.compare(0, sizeof(k.name) - 1, k.name) == 0 &&
+               std::strlen(k.name) == std::min(r.name.size(), sizeof(k.name) - 1);
+      });
+      if (it == agg.end()) {
+        spgemm_kernel_time k;
+        std::memset(&k, 0, sizeof(k));
+        std::strncpy(k.name, r.name.c_str(), sizeof(k.name) - 1);
+        agg.push_back(k);
+        it = agg.end() - 1;
+      }
+      it->launches += 1;
+      it->total_ms += ms;
+      c->ev_pool.push_back(r.a);
+      c->ev_pool.push_back(r.b);
+    }
+    c->prof_recs.clear();
+    for (const auto& k : agg)
+      if (n < max) out[n++] = k;
+  });
+  return n;
+}
+void* spgemm_ctx_stream(spgemm_ctx* c) { return c->main_s; }
+
+spgemm_status spgemm_ctx_synchronize(spgemm_ctx* c) {
+  return guard([&] {
+    DeviceGuard g(c->device);
+    ck(cudaStreamSynchronize(c->main_s), "cudaStreamSynchronize");
+  });
+}
+
+spgemm_status spgemm_preset(int32_t phase, const char* name, spgemm_bin_config* out) {
+  return guard([&] {
+    if (!name || !find_preset(phase, name, out))
+      fail(SPGEMM_INVALID_ARGUMENT,
+           std::string("unknown binning preset '") + (name ? name : "(null)") + "'");
+  });
+}
+
+int32_t spgemm_classify(int64_t value, const spgemm_bin_config* c) { return classify_host(value, *c); }
+
+spgemm_status spgemm_make_plan(const spgemm_bin_config* c, spgemm_plan* out) {
+  return guard([&] { make_plan(*c, out); });
+}
+
+spgemm_status spgemm_pipeline_create(spgemm_ctx* ctx, const spgemm_csr_view* a,
+                                     const spgemm_csr_view* b, const spgemm_options* o,
+                                     spgemm_pipeline** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto* p = new spgemm_pipeline();
+    try {
+      p->ctx = ctx;
+      if (o) p->opts = *o;
+      else spgemm_options_default(&p->opts);
+      spgemm_bin_config sc, nc;
+      if (!find_preset(0, p->opts.sym_preset, &sc))
+        fail(SPGEMM_INVALID_ARGUMENT,
+             std::string("unknown binning preset '") + p->opts.sym_preset + "'");
+      if (!find_preset(1, p->opts.num_preset, &nc))
+        fail(SPGEMM_INVALID_ARGUMENT,
+             std::string("unknown binning preset '") + p->opts.num_preset + "'");
+      if (p->opts.hash_scale <= 0 || p->opts.hash_scale % 2 == 0)
+        fail(SPGEMM_INVALID_ARGUMENT, "hash_scale must be a positive odd integer");
+      p->scale = static_cast<uint32_t>(p->opts.hash_scale);
+      make_plan(sc, &p->sym_plan);
+      make_plan(nc, &p->num_plan);
+      if (a->cols != b->rows)
+        fail(SPGEMM_INVALID_ARGUMENT, "spgemm: a.cols (" + std::to_string(a->cols) +
+                                          ") != b.rows (" + std::to_string(b->rows) + ")");
+      if (p->opts.has_sym_launch_order) apply_launch_order(&p->sym_plan, p->opts.sym_launch_order);
+      if (p->opts.has_num_launch_order) apply_launch_order(&p->num_plan, p->opts.num_launch_order);
+      p->sym_up = to_upper(sc);
+      p->num_up = to_upper(nc);
+      DeviceGuard g(ctx->device);
+      const bool alias = a->rpt == b->rpt && a->col == b->col && a->val == b->val &&
+                         a->rows == b->rows && a->cols == b->cols && a->on_device == b->on_device;
+      stage_input(ctx, a, &p->A, p->owned, &p->a_nnz);
+      if (alias) {
+        p->B = p->A;
+        p->b_nnz = p->a_nnz;
+      } else {
+        stage_input(ctx, b, &p->B, p->owned + 3, &p->b_nnz);
+      }
+      p->M = a->rows;
+      p->avg_b_len = b->rows > 0 ? static_cast<double>(p->b_nnz) / static_cast<double>(b->rows) : 0;
+      for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    } catch (...) {
+      spgemm_pipeline_destroy(p);
+      throw;
+    }
+    *out = p;
+  });
+}
+
+void spgemm_pipeline_destroy(spgemm_pipeline* p) {
+  if (!p) return;
+  if (p->ctx) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->ctx->device);
+    p->release(false);
+    cudaStreamSynchronize(p->ctx->main_s);
+    for (auto& e : p->ev)
+      if (e) cudaEventDestroy(e);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete p;
+}
+
+#define PIPE_STEP(NAME, CALL)                         \
+  spgemm_status NAME(spgemm_pipeline* p) {            \
+    return guard([&] {                                \
+      DeviceGuard g(p->ctx->device);                  \
+      CALL;                                           \
+    });                                               \
+  }
+
+PIPE_STEP(spgemm_pipeline_setup, p->setup())
+PIPE_STEP(spgemm_pipeline_symbolic_binning, p->symbolic_binning())
+PIPE_STEP(spgemm_pipeline_run_symbolic, p->run_symbolic())
+PIPE_STEP(spgemm_pipeline_numeric_binning, p->numeric_binning())
+PIPE_STEP(spgemm_pipeline_run_numeric, p->run_numeric())
+
+spgemm_status spgemm_pipeline_finalize_rpt(spgemm_pipeline* p, int64_t* total) {
+  return guard([&] {
+    DeviceGuard g(p->ctx->device);
+    const int64_t t = p->finalize_rpt();
+    if (total) *total = t;
+  });
+}
+
+spgemm_status spgemm_pipeline_finish(spgemm_pipeline* p, spgemm_report* r) {
+  return guard([&] {
+    DeviceGuard g(p->ctx->device);
+    p->finish(r);
+  });
+}
+
+spgemm_status spgemm_pipeline_run(spgemm_pipeline* p, spgemm_report* r) {
+  return guard([&] {
+    DeviceGuard g(p->ctx->device);
+    p->setup();
+    p->symbolic_binning();
+    p->run_symbolic();
+    p->numeric_binning();
+    p->finalize_rpt();
+    p->run_numeric();
+    p->finish(r);
+  });
+}
+
+spgemm_status spgemm_pipeline_rpt_region(spgemm_pipeline* p, int64_t* host_out) {
+  return guard([&] {
+    DeviceGuard g(p->ctx->device);
+    if (p->stage == spgemm_pipeline::kNew || !p->d_rpt)
+      fail(SPGEMM_LOGIC_ERROR, "spgemm pipeline: rpt_region before setup");
+    ck(cudaMemcpyAsync(host_out, p->d_rpt, static_cast<size_t>(p->M) * 8, cudaMemcpyDeviceToHost,
+                       p->ctx->main_s),
+       "D2H rpt region");
+    ck(cudaStreamSynchronize(p->ctx->main_s), "cudaStreamSynchronize");
+  });
+}
+
+spgemm_status spgemm_pipeline_binning(spgemm_pipeline* p, spgemm_binning_info* info,
+                                      int64_t* bins_host) {
+  return guard([&] {
+    DeviceGuard g(p->ctx->device);
+    if (info) *info = p->bin_info;
+    if (!bins_host || p->M == 0) return;
+    if (p->stage < spgemm_pipeline::kSymBinned || !p->d_arena)
+      fail(SPGEMM_LOGIC_ERROR, "spgemm pipeline: binning not available at this stage");
+    if (p->bin_info.fast_path) {
+      SPG_LAUNCH(p->ctx, "k_iota", p->ctx->main_s,
+                 k_iota<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(p->M, 256), 4096)), 256, 0,
+               p->ctx->main_s>>>(p->d_bins, p->M));
+    }
+    std::vector<int32_t> tmp(static_cast<size_t>(p->M));
+    ck(cudaMemcpyAsync(tmp.data(), p->d_bins, static_cast<size_t>(p->M) * 4,
+                       cudaMemcpyDeviceToHost, p->ctx->main_s),
+       "D2H bins");
+    ck(cudaStreamSynchronize(p->ctx->main_s), "cudaStreamSynchronize");
+    for (int64_t i = 0; i < p->M; ++i) bins_host[i] = tmp[static_cast<size_t>(i)];
+  });
+}
+
+spgemm_status spgemm_pipeline_plan(spgemm_pipeline* p, int32_t phase, spgemm_plan* out) {
+  return guard([&] { *out = phase == 0 ? p->sym_plan : p->num_plan; });
+}
+
+spgemm_status spgemm_pipeline_take_result(spgemm_pipeline* p, spgemm_matrix** c) {
+  *c = nullptr;
+  return guard([&] {
+    if (p->stage != spgemm_pipeline::kDone) fail(SPGEMM_LOGIC_ERROR, "take_result before finish");
+    if (p->result_taken) fail(SPGEMM_LOGIC_ERROR, "result already taken");
+    auto* m = new spgemm_matrix();
+    m->ctx = p->ctx;
+    m->rows = p->M;
+    m->cols = p->B.cols;
+    m->nnz = p->total_nnz;
+    m->rpt = p->d_rpt;
+    m->col = p->d_ccol;
+    m->val = p->d_cval;
+    p->d_rpt = nullptr;
+    p->d_ccol = nullptr;
+    p->d_cval = nullptr;
+    p->result_taken = true;
+    *c = m;
+  });
+}
+
+spgemm_status spgemm_multiply(spgemm_ctx* ctx, const spgemm_csr_view* a, const spgemm_csr_view* b,
+                              const spgemm_options* o, spgemm_matrix** c, spgemm_report* r) {
+  spgemm_pipeline* p = nullptr;
+  spgemm_status st = spgemm_pipeline_create(ctx, a, b, o, &p);
+  if (st != SPGEMM_OK) return st;
+  st = spgemm_pipeline_run(p, r);
+  if (st == SPGEMM_OK) st = spgemm_pipeline_take_result(p, c);
+  std::string keep = g_err;
+  spgemm_pipeline_destroy(p);
+  g_err = keep;
+  return st;
+}
+
+void spgemm_matrix_shape(const spgemm_matrix* m, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  *rows = m->rows;
+  *cols = m->cols;
+  *nnz = m->nnz;
+}
+
+void spgemm_matrix_device_ptrs(const spgemm_matrix* m, const int64_t** rpt, const int32_t** col,
+                               const double** val) {
+  *rpt = m->rpt;
+  *col = m->col;
+  *val = m->val;
+}
+
+spgemm_status spgemm_matrix_download(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t* rpt,
+                                     int32_t* col, double* val) {
+  return guard([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = ctx->main_s;
+    ck(cudaMemcpyAsync(rpt, m->rpt, static_cast<size_t>(m->rows + 1) * 8, cudaMemcpyDeviceToHost, s),
+       "D2H C.rpt");
+    if (m->nnz > 0) {
+      ck(cudaMemcpyAsync(col, m->col, static_cast<size_t>(m->nnz) * 4, cudaMemcpyDeviceToHost, s),
+         "D2H C.col");
+      ck(cudaMemcpyAsync(val, m->val, static_cast<size_t>(m->nnz) * 8, cudaMemcpyDeviceToHost, s),
+         "D2H C.val");
+    }
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+void spgemm_matrix_free(spgemm_matrix* m) {
+  if (!m) return;
+  if (m->ctx) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->ctx->device);
+    dev_free(m->rpt, m->ctx->main_s);
+    dev_free(m->col, m->ctx->main_s);
+    dev_free(m->val, m->ctx->main_s);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete m;
+}
+
+spgemm_status spgemm_compute_nprod(spgemm_ctx* ctx, const spgemm_csr_view* a,
+                                   const spgemm_csr_view* b, int64_t* out_host, int64_t* total) {
+  spgemm_pipeline* p = nullptr;
+  spgemm_status st = spgemm_pipeline_create(ctx, a, b, nullptr, &p);
+  if (st != SPGEMM_OK) return st;
+  st = spgemm_pipeline_setup(p);
+  if (st == SPGEMM_OK && out_host) st = spgemm_pipeline_rpt_region(p, out_host);
+  if (st == SPGEMM_OK && total) *total = p->total_nprod;
+  std::string keep = g_err;
+  spgemm_pipeline_destroy(p);
+  g_err = keep;
+  return st;
+}
+
+spgemm_status spgemm_build_rpt(spgemm_ctx* ctx, int64_t* values, int64_t n, int64_t* total) {
+  return guard([&] {
+    DeviceGuard g(ctx->device);
+    if (n <= 0) {
+      if (total) *total = 0;
+      return;
+    }
+    cudaStream_t s = ctx->main_s;
+    const int64_t ntiles = ceil_div(n, kScanTile);
+    auto* d = static_cast<int64_t*>(dev_alloc(static_cast<size_t>(n) * 8, s));
+    auto* flags = static_cast<int*>(dev_alloc(static_cast<size_t>(ntiles) * 4, s));
+    auto* sums = static_cast<long long*>(dev_alloc(static_cast<size_t>(ntiles) * 16, s));
+    auto* info = static_cast<DevInfo*>(dev_alloc(sizeof(DevInfo), s));
+    ck(cudaMemcpyAsync(d, values, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, s), "H2D");
+    ck(cudaMemsetAsync(flags, 0, static_cast<size_t>(ntiles) * 4, s), "memset");
+    ck(cudaMemsetAsync(info, 0, sizeof(DevInfo), s), "memset");
+    SPG_LAUNCH(ctx, "k_scan", s,
+               k_scan<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(d, n, flags, sums, sums + ntiles, info));
+    ck(cudaMemcpyAsync(values, d, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpyAsync(ctx->h_info, info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (total) *total = ctx->h_info->scan_total;
+    dev_free(d, s);
+    dev_free(flags, s);
+    dev_free(sums, s);
+    dev_free(info, s);
+  });
+}
+
+spgemm_status spgemm_run_binning(spgemm_ctx* ctx, const int64_t* metric, int64_t m,
+                                 const spgemm_bin_config* cfg, int32_t deterministic,
+                                 int64_t* bins_host, spgemm_binning_info* out) {
+  (void)deterministic;  // the device scatter is stable in both modes
+  return guard([&] {
+    DeviceGuard g(ctx->device);
+    if (m < 0) fail(SPGEMM_INVALID_ARGUMENT, "run_binning: bad storage sizes");
+    spgemm_binning_info bi;
+    std::memset(&bi, 0, sizeof(bi));
+    if (m == 0) {
+      bi.fast_path = 1;
+      if (out) *out = bi;
+      return;
+    }
+    cudaStream_t s = ctx->main_s;
+    const BinUpper up = to_upper(*cfg);
+    const int64_t nrb = ceil_div(m, kRowsPerBlock);
+    auto* d_metric = static_cast<int64_t*>(dev_alloc(static_cast<size_t>(m) * 8, s));
+    auto* d_bins = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(m) * 4, s));
+    auto* d_blk = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(nrb) * kNumBins * 4, s));
+    auto* d_info = static_cast<DevInfo*>(dev_alloc(sizeof(DevInfo), s));
+    ck(cudaMemcpyAsync(d_metric, metric, static_cast<size_t>(m) * 8, cudaMemcpyHostToDevice, s), "H2D");
+    ck(cudaMemsetAsync(d_info, 0, sizeof(DevInfo), s), "memset");
+    SPG_LAUNCH(ctx, "k_pass1", s,
+               k_pass1<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(d_metric, m, up, d_blk, d_info));
+    SPG_LAUNCH(ctx, "k_bin_offsets", s,
+               k_bin_offsets<<<1, 1024, 0, s>>>(d_blk, nrb, m, up.u[0], d_info));
+    SPG_LAUNCH(ctx, "k_bin_scatter", s,
+               k_bin_scatter<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(d_metric, m, up, d_blk, d_bins,
+                                                                      d_info));
+    ck(cudaMemcpyAsync(ctx->h_info, d_info, sizeof(DevInfo), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    const DevInfo hi = *ctx->h_info;
+    if (hi.fast_path) {
+      SPG_LAUNCH(ctx, "k_iota", s,
+                 k_iota<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(m, 256), 4096)), 256, 0, s>>>(d_bins, m));
+    }
+    std::vector<int32_t> tmp(static_cast<size_t>(m));
+    ck(cudaMemcpyAsync(tmp.data(), d_bins, static_cast<size_t>(m) * 4, cudaMemcpyDeviceToHost, s),
+       "D2H bins");
+    ck(cudaStreamSynchronize(s), "sync");
+    for (int64_t i = 0; i < m; ++i) bins_host[i] = tmp[static_cast<size_t>(i)];
+    for (int j = 0; j < kNumBins; ++j) {
+      bi.bin_size[j] = hi.bin_size[j];
+      bi.bin_offset[j] = hi.bin_offset[j];
+    }
+    bi.max_metric = hi.max_metric;
+    bi.total_metric = static_cast<int64_t>(hi.total);
+    bi.fast_path = hi.fast_path;
+    if (out) *out = bi;
+    dev_free(d_metric, s);
+    dev_free(d_bins, s);
+    dev_free(d_blk, s);
+    dev_free(d_info, s);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,911 @@
+// kernels.cuh -- sm_100a kernels of the B200-native OpSparse SpGEMM.
+//
+// Reference semantics (paths relative to /root/reference/proj/core):
+//   K1  k_setup_nprod   pipeline.cpp:178-191 (nprod_chunk) + binning.cpp:84-115 (pass 1), fused
+//   K2  k_pass1         binning.cpp:84-115 (binning_pass1) over a device metric
+//   K3  k_bin_offsets   binning.cpp:304-305 + the per-chunk reservation of binning.cpp:205-229
+//   K3  k_bin_scatter   binning.cpp:176-242 (deterministic pass 2: a stable partition by bin)
+//   K5  k_scan          binning.cpp:117-168 (exclusive_sum_inplace) / pipeline.cpp:104-107
+//   K6  k_sym_group / k_sym_block / k_sym_spill
+//                       pipeline.cpp:364-379 -> hash_tables.cpp:94-111 (symbolic_row),
+//                       hash_tables.hpp:62-84 (single-access insert), spill pipeline.cpp:315-348
+//   K7  k_num_group / k_num_block / k_num_global
+//                       pipeline.cpp:380-418 -> hash_tables.cpp:179-201 (numeric_row),
+//                       hash_tables.cpp:125-177 (condense + sort), heap tier pipeline.cpp:396-410
+//
+// Value parity. The reference folds the products of output entry (i, c) as
+// ((0.0 + a[i,p0]*b[p0,c]) + a[i,p1]*b[p1,c]) + ... in A-row order
+// (hash_tables.cpp:182-193, reference.cpp:21-27), with separate multiply and
+// add. Every numeric kernel here walks the A row in order ("ordered steps":
+// one A entry per step, the lanes of the row's group stride the B row, whose
+// columns are distinct, so no two lanes touch the same slot within a step),
+// orders steps with a group/block barrier, and uses __dmul_rn/__dadd_rn (no FMA
+// contraction). The result is bitwise the reference's, independent of bin,
+// preset, launch order or kernel choice.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spgemm_b200 {
+
+constexpr int kNumBins = 8;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBinThreads = 256;                       // binning / pass-1 blocks
+constexpr int kRowsPerThread = 8;
+constexpr int kRowsPerBlock = kBinThreads * kRowsPerThread;  // 2048 rows per row block
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+struct DevCsr {
+  int64_t rows;
+  int64_t cols;
+  const int64_t* __restrict__ rpt;
+  const int32_t* __restrict__ col;
+  const double* __restrict__ val;
+};
+
+struct BinUpper {
+  long long u[kNumBins];
+};
+
+// Device-side scalars of one phase; lives in the metadata arena.
+struct DevInfo {
+  unsigned long long total;      // pass-1 metric total
+  long long max_metric;          // pass-1 max
+  long long bin_size[kNumBins];
+  long long bin_offset[kNumBins];
+  int fast_path;
+  int error;                     // bit 0: numeric count mismatch; bit 1: misbinned
+  unsigned long long spill_count;
+  long long scan_total;
+  long long a_max_row;           // max nnz per A row (input_stats)
+  int tile_counter;
+  int pad_;
+};
+
+constexpr int kErrNumericCount = 1;
+constexpr int kErrTableFull = 2;
+
+// Rows of one bin: either the identity (fast path) or a segment of bins[].
+struct RowList {
+  const int32_t* __restrict__ bins;
+  long long offset;
+  long long count;
+  int identity;
+  __device__ __forceinline__ int64_t row(int64_t idx) const {
+    return identity ? idx : static_cast<int64_t>(bins[offset + idx]);
+  }
+};
+
+__device__ __forceinline__ int classify_bin(long long v, const BinUpper& up) {
+  int j = 0;
+#pragma unroll
+  for (int b = kNumBins - 2; b >= 0; --b) j += v > up.u[b] ? 1 : 0;
+  return j;  // upper[] is strictly increasing, so this is the smallest j with v <= upper[j]
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  if constexpr (G == 32) {
+    return kFull;
+  } else {
+    const unsigned lane = threadIdx.x & 31u;
+    return ((1u << G) - 1u) << (lane & ~(G - 1u));
+  }
+}
+
+template <int G>
+__device__ __forceinline__ int group_sum(int v, unsigned gm) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o, G);
+  return v;
+}
+
+// ------------------------------------------------------------ hash tables
+// Open addressing, h = key*scale masked to the pow2 capacity, linear probe.
+// The plain read doubles as the claim check (hash_tables.hpp:
+// 66-83): a slot that holds a key never changes again, so only an empty slot
+// needs the atomicCAS.
+template <typename Slot>
+__device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, uint32_t scale, uint32_t mask) {
+  uint32_t h = (static_cast<uint32_t>(key) * scale) & mask;
+  while (true) {
+    int32_t cur = *reinterpret_cast<volatile int32_t*>(tab + h);
+    if (cur == key) return 0;
+    if (cur == -1) {
+      cur = atomicCAS(reinterpret_cast<int*>(tab + h), -1, key);
+      if (cur == -1) return 1;
+      if (cur == key) return 0;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ uint32_t num_slot(int32_t* keys, int32_t key, uint32_t scale,
+                                             uint32_t mask) {
+  uint32_t h = (static_cast<uint32_t>(key) * scale) & mask;
+  while (true) {
+    int32_t cur = *reinterpret_cast<volatile int32_t*>(keys + h);
+    if (cur == key) return h;
+    if (cur == -1) {
+      cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, key);
+      if (cur == -1 || cur == key) return h;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// --------------------------------------------------- block-level helpers
+template <int THREADS>
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
+  constexpr int NW = THREADS / 32;
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  long long t = 0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < NW ? red[threadIdx.x] : 0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// Exclusive block scan of one long long per thread; returns the exclusive
+// prefix and writes the block total to *total.
+template <int THREADS>
+__device__ __forceinline__ long long block_exclusive_scan(long long v, long long* red,
+                                                          long long* total) {
+  constexpr int NW = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) red[warp] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    long long w = threadIdx.x < NW ? red[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    if (threadIdx.x < NW) red[threadIdx.x] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  const long long warp_excl = warp > 0 ? red[warp - 1] : 0;
+  *total = red[NW - 1];
+  __syncthreads();
+  return warp_excl + x - v;
+}
+
+// ---------------------------------------------------------------- K1 + K2
+// Shared tail of both pass-1 kernels: per-row-block bin histogram (the
+// per-chunk counts the deterministic pass 2 reserves from), block max/total.
+__device__ __forceinline__ void pass1_finish(int* s_hist, long long mx, unsigned long long tot,
+                                             int32_t* blk_counts, DevInfo* info,
+                                             long long* s_red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    tot += __shfl_xor_sync(kFull, tot, o);
+  }
+  if (lane == 0) {
+    s_red[warp] = mx;
+    s_red[8 + warp] = static_cast<long long>(tot);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long m = 0;
+    unsigned long long t = 0;
+    for (int w = 0; w < kBinThreads / 32; ++w) {
+      m = max(m, s_red[w]);
+      t += static_cast<unsigned long long>(s_red[8 + w]);
+    }
+    atomicMax(&info->max_metric, m);
+    atomicAdd(&info->total, t);
+  }
+  if (threadIdx.x < kNumBins) blk_counts[blockIdx.x * kNumBins + threadIdx.x] = s_hist[threadIdx.x];
+}
+
+// K1: nprod[i] = sum over A(i,:) of nnz(B(k,:)), written into C.rpt[0..M);
+// fused with the symbolic pass-1 histogram and input_stats' max row length.
+// Rows are read coalesced (thread per row); rows longer than 32 entries are
+// summed cooperatively by their warp so power-law rows do not serialise.
+__global__ void __launch_bounds__(kBinThreads)
+    k_setup_nprod(DevCsr A, const int64_t* __restrict__ brpt, int64_t* __restrict__ rpt,
+                  int64_t M, BinUpper up, int32_t* __restrict__ blk_counts, DevInfo* info) {
+  __shared__ int s_hist[kNumBins];
+  __shared__ long long s_red[16];
+  if (threadIdx.x < kNumBins) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  long long mx = 0, amax = 0;
+  unsigned long long tot = 0;
+#pragma unroll 1
+  for (int it = 0; it < kRowsPerThread; ++it) {
+    const int64_t row = base + it * kBinThreads + threadIdx.x;
+    const bool valid = row < M;
+    int64_t a0 = 0, a1 = 0;
+    if (valid) {
+      a0 = A.rpt[row];
+      a1 = A.rpt[row + 1];
+    }
+    const bool longrow = (a1 - a0) > 32;
+    long long n = 0;
+    if (!longrow) {
+      for (int64_t p = a0; p < a1; ++p) {
+        const int32_t k = A.col[p];
+        n += brpt[k + 1] - brpt[k];
+      }
+    }
+    unsigned lm = __ballot_sync(kFull, longrow);
+    while (lm) {
+      const int src = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const int64_t s0 = __shfl_sync(kFull, a0, src), s1 = __shfl_sync(kFull, a1, src);
+      long long part = 0;
+      for (int64_t p = s0 + lane; p < s1; p += 32) {
+        const int32_t k = A.col[p];
+        part += brpt[k + 1] - brpt[k];
+      }
+      part = warp_sum(part);
+      if (lane == src) n = part;
+    }
+    if (valid) {
+      rpt[row] = n;
+      atomicAdd(&s_hist[classify_bin(n, up)], 1);
+      mx = max(mx, n);
+      tot += static_cast<unsigned long long>(n);
+      amax = max(amax, static_cast<long long>(a1 - a0));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = max(amax, __shfl_xor_sync(kFull, amax, o));
+  if (lane == 0 && amax > 0) atomicMax(&info->a_max_row, amax);
+  __syncthreads();
+  pass1_finish(s_hist, mx, tot, blk_counts, info, s_red);
+  if (blockIdx.x == 0 && threadIdx.x == 0) rpt[M] = 0;
+}
+
+// K2: pass 1 over an arbitrary device metric (numeric phase: per-row nnz).
+__global__ void __launch_bounds__(kBinThreads)
+    k_pass1(const int64_t* __restrict__ metric, int64_t M, BinUpper up,
+            int32_t* __restrict__ blk_counts, DevInfo* info) {
+  __shared__ int s_hist[kNumBins];
+  __shared__ long long s_red[16];
+  if (threadIdx.x < kNumBins) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  long long mx = 0;
+  unsigned long long tot = 0;
+#pragma unroll
+  for (int it = 0; it < kRowsPerThread; ++it) {
+    const int64_t row = base + it * kBinThreads + threadIdx.x;
+    if (row < M) {
+      const long long v = metric[row];
+      atomicAdd(&s_hist[classify_bin(v, up)], 1);
+      mx = max(mx, v);
+      tot += static_cast<unsigned long long>(v);
+    }
+  }
+  __syncthreads();
+  pass1_finish(s_hist, mx, tot, blk_counts, info, s_red);
+}
+
+// K3a: bin sizes, bin offsets (exclusive sum over bins, binning.cpp:304-305),
+// fast-path flag, and the per-row-block write cursors in row-block order
+// (the deterministic reservation of binning.cpp:220-229). One block.
+__global__ void __launch_bounds__(1024)
+    k_bin_offsets(int32_t* __restrict__ blk_counts, int64_t nrb, int64_t M, long long upper0,
+                  DevInfo* info) {
+  __shared__ long long s_red[32];
+  __shared__ long long s_bin[kNumBins];
+  long long local[kNumBins];
+#pragma unroll
+  for (int j = 0; j < kNumBins; ++j) local[j] = 0;
+  for (int64_t b = threadIdx.x; b < nrb; b += 1024) {
+#pragma unroll
+    for (int j = 0; j < kNumBins; ++j) local[j] += blk_counts[b * kNumBins + j];
+  }
+#pragma unroll 1
+  for (int j = 0; j < kNumBins; ++j) {
+    const long long t = block_sum_ll<1024>(local[j], s_red);
+    if (threadIdx.x == 0) s_bin[j] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int j = 0; j < kNumBins; ++j) {
+      info->bin_size[j] = s_bin[j];
+      info->bin_offset[j] = run;
+      run += s_bin[j];
+    }
+    info->fast_path = (M == 0 || info->max_metric <= upper0) ? 1 : 0;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int j = 0; j < kNumBins; ++j) {
+    long long carry = 0;
+    for (int j2 = 0; j2 < j; ++j2) carry += s_bin[j2];
+    for (int64_t t0 = 0; t0 < nrb; t0 += 1024) {
+      const int64_t b = t0 + threadIdx.x;
+      const long long v = b < nrb ? blk_counts[b * kNumBins + j] : 0;
+      long long tile_total;
+      const long long ex = block_exclusive_scan<1024>(v, s_red, &tile_total);
+      if (b < nrb) blk_counts[b * kNumBins + j] = static_cast<int32_t>(carry + ex);
+      carry += tile_total;
+    }
+  }
+}
+
+// K3b: scatter row ids into their bin segments. Within a row block the ids
+// are ranked with warp ballots in ascending row order, so every segment lists
+// its rows ascending: exactly the reference's deterministic layout
+// (binning.cpp:205-241), whatever the chunk size. Skipped on the fast path.
+__global__ void __launch_bounds__(kBinThreads)
+    k_bin_scatter(const int64_t* __restrict__ metric, int64_t M, BinUpper up,
+                  const int32_t* __restrict__ blk_offsets, int32_t* __restrict__ bins,
+                  const DevInfo* info) {
+  if (info->fast_path) return;
+  constexpr int NW = kBinThreads / 32;
+  __shared__ int s_wcnt[NW][kNumBins];
+  __shared__ int s_run[kNumBins];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < kNumBins) s_run[threadIdx.x] = blk_offsets[blockIdx.x * kNumBins + threadIdx.x];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll 1
+  for (int it = 0; it < kRowsPerThread; ++it) {
+    const int64_t row = base + it * kBinThreads + threadIdx.x;
+    const bool valid = row < M;
+    const int bin = valid ? classify_bin(metric[row], up) : -1;
+    int rank = 0;
+#pragma unroll
+    for (int j = 0; j < kNumBins; ++j) {
+      const unsigned m = __ballot_sync(kFull, bin == j);
+      if (bin == j) rank = __popc(m & lt);
+      if (lane == j) s_wcnt[warp][j] = __popc(m);
+    }
+    __syncthreads();
+    if (valid) {
+      int pos = s_run[bin] + rank;
+      for (int w = 0; w < warp; ++w) pos += s_wcnt[w][bin];
+      bins[pos] = static_cast<int32_t>(row);
+    }
+    __syncthreads();
+    if (threadIdx.x < kNumBins) {
+      int add = 0;
+      for (int w = 0; w < NW; ++w) add += s_wcnt[w][threadIdx.x];
+      s_run[threadIdx.x] += add;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_iota(int32_t* out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int32_t>(i);
+}
+
+// K5: single-pass in-place exclusive scan (decoupled look-back) of n int64.
+// Tiles are claimed in launch order through an atomic ticket so look-back
+// always waits on tiles that are already running. A tile publishes its
+// aggregate (flag 1) and later its inclusive prefix (flag 2) in separate
+// slots, so a reader never sees one overwritten by the other.
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan(int64_t* __restrict__ data, int64_t n, int* __restrict__ flags,
+           long long* __restrict__ aggs, long long* __restrict__ incl, DevInfo* info) {
+  __shared__ int s_tile;
+  __shared__ long long s_red[32];
+  __shared__ long long s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&info->tile_counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = static_cast<int64_t>(tile) * kScanTile + threadIdx.x * kScanItems;
+  long long v[kScanItems];
+  long long tsum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < n) ? data[base + i] : 0;
+    tsum += v[i];
+  }
+  long long agg;
+  const long long texcl = block_exclusive_scan<kScanThreads>(tsum, s_red, &agg);
+  if (threadIdx.x == 0) {
+    long long excl = 0;
+    if (tile == 0) {
+      incl[0] = agg;
+      __threadfence();
+      atomicExch(&flags[0], 2);
+    } else {
+      aggs[tile] = agg;
+      __threadfence();
+      atomicExch(&flags[tile], 1);
+      int p = tile - 1;
+      while (true) {
+        int f;
+        do {
+          f = *reinterpret_cast<volatile int*>(&flags[p]);
+        } while (f == 0);
+        __threadfence();
+        if (f == 2) {
+          excl += *reinterpret_cast<volatile long long*>(&incl[p]);
+          break;
+        }
+        excl += *reinterpret_cast<volatile long long*>(&aggs[p]);
+        --p;
+      }
+      incl[tile] = excl + agg;
+      __threadfence();
+      atomicExch(&flags[tile], 2);
+    }
+    s_excl = excl;
+    if ((static_cast<int64_t>(tile) + 1) * kScanTile >= n) info->scan_total = excl + agg;
+  }
+  __syncthreads();
+  long long run = s_excl + texcl;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) data[base + i] = run;
+    run += v[i];
+  }
+}
+
+// --------------------------------------------------------- K6 symbolic
+// Group kernel: G lanes per output row, NGRP rows in flight per block, one
+// pow2 table of T int32 slots per row in shared memory. Persistent over the
+// bin's rows (grid = resident blocks). The A row is walked entry by entry and
+// the group's lanes stride the entry's B row.
+template <int G, int T, int NGRP>
+__global__ void __launch_bounds__(G* NGRP)
+    k_sym_group(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + (threadIdx.x / G) * T;
+  const int lane = threadIdx.x % G;
+  const unsigned gm = group_mask<G>();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * NGRP;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * NGRP + threadIdx.x / G; idx < rl.count;
+       idx += stride) {
+    const int64_t row = rl.row(idx);
+    if (rpt[row] == 0) continue;  // no products: nnz 0 (pipeline.cpp:368-371)
+#pragma unroll 4
+    for (int s = lane; s < T; s += G) tab[s] = -1;
+    __syncwarp(gm);
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    int cnt = 0;
+    for (int64_t p = a0; p < a1; ++p) {
+      const int32_t k = A.col[p];
+      const int64_t b1 = B.rpt[k + 1];
+      for (int64_t q = B.rpt[k] + lane; q < b1; q += G) cnt += sym_insert(tab, B.col[q], scale, T - 1);
+    }
+    cnt = group_sum<G>(cnt, gm);
+    __syncwarp(gm);
+    if (lane == 0) rpt[row] = cnt;
+  }
+}
+
+// Block kernel: one row per block iteration, warps take A entries, lanes
+// stride B rows. SPILL (the last bin): the fixed table aborts a row once its
+// distinct count exceeds the reference's 0.8*24575 = 19660 threshold
+// (hash_tables.hpp:18-21) and queues it for k_sym_spill.
+template <int T, int THREADS, bool SPILL>
+__global__ void __launch_bounds__(THREADS)
+    k_sym_block(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale,
+                int32_t* __restrict__ spill_ids, DevInfo* info, int thresh) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw);
+  __shared__ int s_cnt, s_abort;
+  __shared__ long long s_red[32];
+  constexpr int NW = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
+    const int64_t row = rl.row(idx);
+    if (rpt[row] == 0) continue;
+    for (int s = threadIdx.x; s < T; s += THREADS) tab[s] = -1;
+    if (threadIdx.x == 0) {
+      s_cnt = 0;
+      s_abort = 0;
+    }
+    __syncthreads();
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    int cnt = 0;
+    for (int64_t p = a0 + warp; p < a1; p += NW) {
+      const int32_t k = A.col[p];
+      const int64_t b0 = B.rpt[k], b1 = B.rpt[k + 1];
+      for (int64_t qb = b0; qb < b1; qb += 32) {
+        const int64_t q = qb + lane;
+        const int nw = q < b1 ? sym_insert(tab, B.col[q], scale, T - 1) : 0;
+        if constexpr (SPILL) {
+          const unsigned bal = __ballot_sync(kFull, nw);
+          int abort = 0;
+          if (lane == 0) {
+            if (bal) {
+              const int c = __popc(bal);
+              if (atomicAdd(&s_cnt, c) + c > thresh) s_abort = 1;
+            }
+            abort = *reinterpret_cast<volatile int*>(&s_abort);
+          }
+          if (__shfl_sync(kFull, abort, 0)) goto row_done;
+        } else {
+          cnt += nw;
+        }
+      }
+    }
+  row_done:
+    if constexpr (SPILL) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (s_abort) {
+          const unsigned long long i = atomicAdd(&info->spill_count, 1ull);
+          spill_ids[i] = static_cast<int32_t>(row);
+        } else {
+          rpt[row] = s_cnt;
+        }
+      }
+      __syncthreads();
+    } else {
+      const long long total = block_sum_ll<THREADS>(cnt, s_red);
+      if (threadIdx.x == 0) rpt[row] = total;
+    }
+  }
+}
+
+// Spilled rows (pipeline.cpp:315-348, hash_tables.cpp:113-123): recount with a
+// global-memory table. Instead of one heap table per row, each resident block
+// reuses one region of a pool; the row's table is bit_ceil(2*min(nprod, cols)).
+__global__ void __launch_bounds__(1024)
+    k_sym_spill(DevCsr A, DevCsr B, int64_t* __restrict__ rpt, const int32_t* __restrict__ spill_ids,
+                const DevInfo* info, int32_t* __restrict__ pool, int64_t slots_per_block,
+                uint32_t scale) {
+  __shared__ long long s_red[32];
+  int32_t* tab = pool + static_cast<int64_t>(blockIdx.x) * slots_per_block;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long count = static_cast<long long>(info->spill_count);
+  for (long long idx = blockIdx.x; idx < count; idx += gridDim.x) {
+    const int64_t row = spill_ids[idx];
+    const long long nprod = rpt[row];
+    long long want = 2 * min(nprod, static_cast<long long>(B.cols));
+    long long t = 2;
+    while (t < want) t <<= 1;
+    if (t > slots_per_block) t = slots_per_block;
+    const uint32_t mask = static_cast<uint32_t>(t - 1);
+    for (long long s = threadIdx.x; s < t; s += 1024) tab[s] = -1;
+    __syncthreads();
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    int cnt = 0;
+    for (int64_t p = a0 + warp; p < a1; p += 32) {
+      const int32_t k = A.col[p];
+      const int64_t b1 = B.rpt[k + 1];
+      for (int64_t q = B.rpt[k] + lane; q < b1; q += 32) cnt += sym_insert(tab, B.col[q], scale, mask);
+    }
+    const long long total = block_sum_ll<1024>(cnt, s_red);
+    if (threadIdx.x == 0) rpt[row] = total;
+  }
+}
+
+// ---------------------------------------------------------- K7 numeric
+// Sort of (col << 32 | slot) keys held E per lane across a G-lane group.
+template <int G, int E>
+__device__ __forceinline__ void group_bitonic(unsigned long long (&v)[E], int lane, unsigned gm) {
+  constexpr int N = G * E;
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lj = j / E;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int e = lane * E + i;
+          const unsigned long long other = __shfl_xor_sync(gm, v[i], lj, G);
+          const bool up = (e & k) == 0;
+          const bool lower = (e & j) == 0;
+          v[i] = (lower == up) ? min(v[i], other) : max(v[i], other);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int pi = i ^ j;
+          if (pi > i) {
+            const int e = lane * E + i;
+            const bool up = (e & k) == 0;
+            const unsigned long long a = v[i], b = v[pi];
+            const bool sw = up ? (a > b) : (a < b);
+            v[i] = sw ? b : a;
+            v[pi] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Group kernel: G lanes per row; per group T key slots + T fp64 values +
+// G*E packed sort keys in shared memory. Ordered steps over the A row (see
+// the header comment), then condense (hash_tables.cpp:125-135), a group
+// bitonic sort by column, and the write of C(i,:) at rpt[i].
+template <int G, int T, int E, int NGRP>
+__global__ void __launch_bounds__(G* NGRP)
+    k_num_group(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+                int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
+                DevInfo* info) {
+  constexpr int NMAX = G * E;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int grp = threadIdx.x / G;
+  unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * (T * 12 + NMAX * 8);
+  double* vals = reinterpret_cast<double*>(gbase);
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(gbase + T * 8);
+  int32_t* keys = reinterpret_cast<int32_t*>(gbase + T * 8 + NMAX * 8);
+  const int lane = threadIdx.x % G;
+  const unsigned gm = group_mask<G>();
+  const unsigned gshift = (threadIdx.x & 31u) & ~(G - 1u);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * NGRP;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * NGRP + grp; idx < rl.count; idx += stride) {
+    const int64_t row = rl.row(idx);
+    const int64_t base = rpt[row];
+    const int n = static_cast<int>(rpt[row + 1] - base);
+    if (n == 0) continue;
+#pragma unroll 4
+    for (int s = lane; s < T; s += G) {
+      keys[s] = -1;
+      vals[s] = 0.0;
+    }
+    __syncwarp(gm);
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    for (int64_t p = a0; p < a1; ++p) {
+      const int32_t k = A.col[p];
+      const double av = A.val[p];
+      const int64_t b1 = B.rpt[k + 1];
+      for (int64_t q = B.rpt[k] + lane; q < b1; q += G) {
+        const double x = __dmul_rn(av, B.val[q]);
+        const uint32_t s = num_slot(keys, B.col[q], scale, T - 1);
+        vals[s] = __dadd_rn(vals[s], x);
+      }
+      __syncwarp(gm);
+    }
+    int run = 0;
+#pragma unroll 4
+    for (int s0 = 0; s0 < T; s0 += G) {
+      const int s = s0 + lane;
+      const int32_t key = keys[s];
+      const bool occ = key != -1;
+      const unsigned bal = __ballot_sync(gm, occ) >> gshift;
+      if (occ)
+        packed[run + __popc(bal & ((1u << lane) - 1u))] =
+            (static_cast<unsigned long long>(static_cast<uint32_t>(key)) << 32) | static_cast<uint32_t>(s);
+      run += __popc(bal);
+    }
+    if (run != n && lane == 0) atomicOr(&info->error, kErrNumericCount);
+    __syncwarp(gm);
+    unsigned long long v[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int e = lane * E + i;
+      v[i] = e < n ? packed[e] : ~0ull;
+    }
+    group_bitonic<G, E>(v, lane, gm);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int e = lane * E + i;
+      if (e < n) {
+        ccol[base + e] = static_cast<int32_t>(v[i] >> 32);
+        cval[base + e] = vals[static_cast<uint32_t>(v[i])];
+      }
+    }
+    __syncwarp(gm);
+  }
+}
+
+// In-place bitonic sort of np (pow2) packed keys in shared memory by a block.
+template <int THREADS>
+__device__ __forceinline__ void block_bitonic_smem(unsigned long long* a, int np) {
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (np >> 1); i += THREADS) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        const int hi = lo + j;
+        const bool up = (lo & k) == 0;
+        const unsigned long long x = a[lo], y = a[hi];
+        if ((x > y) == up) {
+          a[lo] = y;
+          a[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Block kernel: one row per block iteration, table of T slots in shared
+// memory, ordered steps with a block barrier per A entry.
+template <int T, int THREADS, int NMAX>
+__global__ void __launch_bounds__(THREADS)
+    k_num_block(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+                int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
+                DevInfo* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* vals = reinterpret_cast<double*>(smem_raw);
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(smem_raw + T * 8);
+  int32_t* keys = reinterpret_cast<int32_t*>(smem_raw + T * 8 + NMAX * 8);
+  __shared__ long long s_red[32];
+  constexpr int PER = T / THREADS;
+  for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
+    const int64_t row = rl.row(idx);
+    const int64_t base = rpt[row];
+    const int n = static_cast<int>(rpt[row + 1] - base);
+    if (n == 0) continue;
+    for (int s = threadIdx.x; s < T; s += THREADS) {
+      keys[s] = -1;
+      vals[s] = 0.0;
+    }
+    __syncthreads();
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    for (int64_t p = a0; p < a1; ++p) {
+      const int32_t k = A.col[p];
+      const double av = A.val[p];
+      const int64_t b1 = B.rpt[k + 1];
+      for (int64_t q = B.rpt[k] + threadIdx.x; q < b1; q += THREADS) {
+        const double x = __dmul_rn(av, B.val[q]);
+        const uint32_t s = num_slot(keys, B.col[q], scale, T - 1);
+        vals[s] = __dadd_rn(vals[s], x);
+      }
+      __syncthreads();
+    }
+    // condense: each thread owns PER consecutive slots
+    int mine = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) mine += keys[threadIdx.x * PER + i] != -1;
+    long long total;
+    long long pos = block_exclusive_scan<THREADS>(mine, s_red, &total);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int s = threadIdx.x * PER + i;
+      const int32_t key = keys[s];
+      if (key != -1)
+        packed[pos++] = (static_cast<unsigned long long>(static_cast<uint32_t>(key)) << 32) |
+                        static_cast<uint32_t>(s);
+    }
+    if (threadIdx.x == 0 && total != n) atomicOr(&info->error, kErrNumericCount);
+    int np = 1;
+    while (np < n) np <<= 1;
+    for (int e = n + threadIdx.x; e < np; e += THREADS) packed[e] = ~0ull;
+    __syncthreads();
+    block_bitonic_smem<THREADS>(packed, np);
+    for (int e = threadIdx.x; e < n; e += THREADS) {
+      const unsigned long long v = packed[e];
+      ccol[base + e] = static_cast<int32_t>(v >> 32);
+      cval[base + e] = vals[static_cast<uint32_t>(v)];
+    }
+    __syncthreads();
+  }
+}
+
+// Heap tier (pipeline.cpp:396-410): rows past the largest shared tier.
+// Table of bit_ceil(2*nnz) slots in a per-block region of a global pool,
+// ordered steps, then the row's columns are ranked without a comparison
+// sort: a bitmap over a window of the column range plus an exclusive popcount
+// scan gives each entry its output position directly (columns are distinct).
+constexpr int kGlobalThreads = 512;
+__global__ void __launch_bounds__(kGlobalThreads)
+    k_num_global(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
+                 int32_t* __restrict__ pool_keys, double* __restrict__ pool_vals,
+                 uint32_t* __restrict__ pool_bits, int64_t slots_per_block, int64_t words_per_block,
+                 DevInfo* info) {
+  __shared__ long long s_red[32];
+  __shared__ int s_min, s_max;
+  int32_t* keys = pool_keys + static_cast<int64_t>(blockIdx.x) * slots_per_block;
+  double* vals = pool_vals + static_cast<int64_t>(blockIdx.x) * slots_per_block;
+  uint32_t* bits = pool_bits + static_cast<int64_t>(blockIdx.x) * 2 * words_per_block;
+  uint32_t* pref = bits + words_per_block;
+  for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
+    const int64_t row = rl.row(idx);
+    const int64_t base = rpt[row];
+    const int64_t n = rpt[row + 1] - base;
+    if (n == 0) continue;
+    int64_t t = 2;
+    while (t < 2 * n) t <<= 1;
+    if (t > slots_per_block) t = slots_per_block;
+    const uint32_t mask = static_cast<uint32_t>(t - 1);
+    for (int64_t s = threadIdx.x; s < t; s += kGlobalThreads) {
+      keys[s] = -1;
+      vals[s] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+      s_min = 0x7fffffff;
+      s_max = -1;
+    }
+    __syncthreads();
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    for (int64_t p = a0; p < a1; ++p) {
+      const int32_t k = A.col[p];
+      const double av = A.val[p];
+      const int64_t b1 = B.rpt[k + 1];
+      for (int64_t q = B.rpt[k] + threadIdx.x; q < b1; q += kGlobalThreads) {
+        const double x = __dmul_rn(av, B.val[q]);
+        const uint32_t s = num_slot(keys, B.col[q], scale, mask);
+        vals[s] = __dadd_rn(vals[s], x);
+      }
+      __syncthreads();
+    }
+    int lmin = 0x7fffffff, lmax = -1;
+    for (int64_t s = threadIdx.x; s < t; s += kGlobalThreads) {
+      const int32_t key = keys[s];
+      if (key != -1) {
+        lmin = min(lmin, key);
+        lmax = max(lmax, key);
+      }
+    }
+    atomicMin(&s_min, lmin);
+    atomicMax(&s_max, lmax);
+    __syncthreads();
+    const int64_t kmin = s_min, kmax = s_max;
+    const int64_t wbits = words_per_block * 32;
+    int64_t written = 0;
+    for (int64_t w0 = kmin; w0 <= kmax; w0 += wbits) {
+      const int64_t span = min(wbits, kmax - w0 + 1);
+      const int64_t nwords = (span + 31) / 32;
+      for (int64_t w = threadIdx.x; w < nwords; w += kGlobalThreads) bits[w] = 0u;
+      __syncthreads();
+      for (int64_t s = threadIdx.x; s < t; s += kGlobalThreads) {
+        const int32_t key = keys[s];
+        if (key != -1 && key >= w0 && key < w0 + span) {
+          const int64_t off = key - w0;
+          atomicOr(&bits[off >> 5], 1u << (off & 31));
+        }
+      }
+      __syncthreads();
+      // exclusive popcount scan over nwords, each thread a contiguous chunk
+      const int64_t per = (nwords + kGlobalThreads - 1) / kGlobalThreads;
+      const int64_t w_lo = min(nwords, threadIdx.x * per), w_hi = min(nwords, w_lo + per);
+      long long mine = 0;
+      for (int64_t w = w_lo; w < w_hi; ++w) mine += __popc(bits[w]);
+      long long wtotal;
+      long long run = block_exclusive_scan<kGlobalThreads>(mine, s_red, &wtotal);
+      for (int64_t w = w_lo; w < w_hi; ++w) {
+        pref[w] = static_cast<uint32_t>(run);
+        run += __popc(bits[w]);
+      }
+      __syncthreads();
+      for (int64_t s = threadIdx.x; s < t; s += kGlobalThreads) {
+        const int32_t key = keys[s];
+        if (key != -1 && key >= w0 && key < w0 + span) {
+          const int64_t off = key - w0;
+          const uint32_t word = bits[off >> 5];
+          const int64_t pos =
+              written + pref[off >> 5] + __popc(word & ((1u << (off & 31)) - 1u));
+          ccol[base + pos] = key;
+          cval[base + pos] = vals[s];
+        }
+      }
+      written += wtotal;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && written != n) atomicOr(&info->error, kErrNumericCount);
+    __syncthreads();
+  }
+}
+
+}  // namespace spgemm_b200

@@ -1,0 +1,72 @@
+"""GPU parity on the BASELINE.json config families.
+
+Small instances are checked entry-for-entry (bitwise) against the C oracle;
+the full-size stencil configs are checked against the oracle too (they finish
+in seconds on the host), and carry the published statistics as known answers.
+"""
+import numpy as np
+import pytest
+
+from helpers import assert_matches_oracle
+from paper_2206_07244_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(sg, oracle, a, b, **kw):
+    out = sg.multiply(a, b, sg.SpgemmOptions(**kw))
+    exp = oracle.spgemm(a, b)
+    assert_matches_oracle(out.c, exp)
+    return out
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_small_config_square(sg, oracle, cfg):
+    a, b = S.config_matrices(cfg, small=True)
+    _check(sg, oracle, a, b)
+    _check(sg, oracle, S.random_values(a, 7), S.random_values(b, 7))
+
+
+def test_small_rap_chain(sg, oracle):
+    a, p, r = S.config_matrices(4, small=True)
+    ap = _check(sg, oracle, a, p).c
+    _check(sg, oracle, r, ap)
+
+
+@pytest.mark.parametrize("scale", [12, 14])
+def test_rmat_mid(sg, oracle, scale):
+    a = S.random_values(S.rmat(scale, 16, seed=scale), 3)
+    out = _check(sg, oracle, a, a)
+    assert out.stats.total_nprod == oracle.compute_nprod(a, a)[1]
+
+
+def test_config1_full_known_answer(sg, oracle):
+    a, _ = S.config_matrices(1)
+    out = _check(sg, oracle, a, a)
+    assert out.stats.total_nprod == 26_177_544 and out.stats.nnz_of_product == 13_611_012
+
+
+@pytest.mark.slow
+def test_config2_full_known_answer(sg, oracle):
+    a, _ = S.config_matrices(2)
+    out = _check(sg, oracle, a, a)
+    assert out.stats.total_nprod == 1_489_355_288 and out.stats.nnz_of_product == 254_840_104
+
+
+def test_config4_full_known_answer(sg, oracle):
+    a, p, r = S.config_matrices(4)
+    ap = _check(sg, oracle, a, p)
+    assert ap.stats.total_nprod == 48_556_211 and ap.stats.nnz_of_product == 20_757_689
+    rap = _check(sg, oracle, r, ap.c)
+    assert rap.stats.total_nprod == 69_839_855 and rap.stats.nnz_of_product == 6_859_000
+
+
+def test_device_resident_inputs(sg, oracle):
+    a, _ = S.config_matrices(2, small=True)
+    a = S.random_values(a, 11)
+    d = a.to_device()
+    dm, rep = sg.multiply_device(d, d)
+    c = dm.download()
+    dm.free()
+    assert_matches_oracle(c, oracle.spgemm(a, a))
+    assert rep.stats.total_nprod == oracle.compute_nprod(a, a)[1]
