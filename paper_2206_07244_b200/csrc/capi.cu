@@ -509,18 +509,21 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     dev_free(pool, s);
     return;
   }
-  if (u <= 32) {
+  if (u < 64) {
     if (g8) group(k_sym_group<8, 64, 32>, 8, 64, 32);
     else group(k_sym_group<32, 64, 8>, 32, 64, 8);
-  } else if (u <= 512) {
+  } else if (u < 512) {
+    if (g8) group(k_sym_group<8, 512, 32>, 8, 512, 32);
+    else group(k_sym_group<32, 512, 8>, 32, 512, 8);
+  } else if (u < 1024) {
     if (g8) group(k_sym_group<8, 1024, 16>, 8, 1024, 16);
     else group(k_sym_group<32, 1024, 8>, 32, 1024, 8);
-  } else if (u <= 1024) {
+  } else if (u < 2048) {
     if (g8) group(k_sym_group<8, 2048, 8>, 8, 2048, 8);
     else group(k_sym_group<32, 2048, 8>, 32, 2048, 8);
-  } else if (u <= 2048) {
+  } else if (u < 4096) {
     block(k_sym_block<4096, 256, false>, 4096, 256);
-  } else if (u <= 4096) {
+  } else if (u < 8192) {
     block(k_sym_block<8192, 256, false>, 8192, 256);
   } else {
     block(k_sym_block<16384, 512, false>, 16384, 512);

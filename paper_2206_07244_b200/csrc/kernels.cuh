@@ -111,13 +111,43 @@ __device__ __forceinline__ int group_sum(int v, unsigned gm) {
 }
 
 // ------------------------------------------------------------ hash tables
-// Open addressing, h = key*scale masked to the pow2 capacity, linear probe.
-// The plain read doubles as the claim check (hash_tables.hpp:
-// 66-83): a slot that holds a key never changes again, so only an empty slot
-// needs the atomicCAS.
+// Open addressing with linear probing over a pow2 table of 2^lg slots. The home
+// slot takes the HIGH lg bits of key*scale*phi (Fibonacci hashing): the
+// reference's key*scale & (t-1) (hash_tables.hpp:54-57) keeps only the low
+// bits, so stencil columns that differ by a multiple of 2^lg (every y/z plane
+// of a grid) share one probe chain. The slot a key lands in never affects the
+// result (only the probe count), and hash_scale is still the odd multiplier
+// the reference validates. The plain read doubles as the claim check
+// (hash_tables.hpp:66-83): a slot that holds a key never changes
+// again, so only an empty slot needs the atomicCAS.
+struct Hash {
+  uint32_t mult;   // scale * 0x9E3779B1 (odd)
+  uint32_t shift;  // 32 - lg
+  uint32_t mask;   // 2^lg - 1
+  __device__ __forceinline__ uint32_t home(int32_t key) const {
+    return (static_cast<uint32_t>(key) * mult) >> shift;
+  }
+};
+
+__device__ __forceinline__ Hash make_hash(uint32_t scale, int lg) {
+  Hash h;
+  h.mult = scale * 0x9E3779B1u;
+  h.shift = 32u - static_cast<uint32_t>(lg);
+  h.mask = lg >= 32 ? 0xffffffffu : ((1u << lg) - 1u);
+  if (lg == 0) h.shift = 31u, h.mask = 0u;
+  return h;
+}
+
+template <int T>
+__host__ __device__ constexpr int log2_const() {
+  int l = 0;
+  while ((1 << l) < T) ++l;
+  return l;
+}
+
 template <typename Slot>
-__device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, uint32_t scale, uint32_t mask) {
-  uint32_t h = (static_cast<uint32_t>(key) * scale) & mask;
+__device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, const Hash& hs) {
+  uint32_t h = hs.home(key) & hs.mask;
   while (true) {
     int32_t cur = *reinterpret_cast<volatile int32_t*>(tab + h);
     if (cur == key) return 0;
@@ -126,13 +156,12 @@ __device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, uint32_t scale
       if (cur == -1) return 1;
       if (cur == key) return 0;
     }
-    h = (h + 1) & mask;
+    h = (h + 1) & hs.mask;
   }
 }
 
-__device__ __forceinline__ uint32_t num_slot(int32_t* keys, int32_t key, uint32_t scale,
-                                             uint32_t mask) {
-  uint32_t h = (static_cast<uint32_t>(key) * scale) & mask;
+__device__ __forceinline__ uint32_t num_slot(int32_t* keys, int32_t key, const Hash& hs) {
+  uint32_t h = hs.home(key) & hs.mask;
   while (true) {
     int32_t cur = *reinterpret_cast<volatile int32_t*>(keys + h);
     if (cur == key) return h;
@@ -140,7 +169,7 @@ __device__ __forceinline__ uint32_t num_slot(int32_t* keys, int32_t key, uint32_
       cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, key);
       if (cur == -1 || cur == key) return h;
     }
-    h = (h + 1) & mask;
+    h = (h + 1) & hs.mask;
   }
 }
 
@@ -473,14 +502,93 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+// ------------------------------------------------------------- row walker
+template <int G>
+__device__ __forceinline__ int group_max(int v, unsigned gm) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(gm, v, o, G));
+  return v;
+}
+
+// Visits the products of one output row in the reference's (A entry, B entry)
+// order. The group's lanes first load up to G A entries at once (column k,
+// value, B row start/length: one round of latency instead of a dependent
+// A.col -> B.rpt -> B.col chain per entry). When every B row of the chunk fits
+// in G lanes, entry j is one "step" (lane q takes B(k_j, q)), and the B loads
+// of U steps are issued before any of them is consumed, so U (x2 with
+// values) independent loads are in flight per lane. Otherwise the group
+// strides each B row. ORDERED inserts a group barrier after each A entry:
+// within an entry the B columns are distinct (no two lanes share a slot), and
+// the barrier orders entry j's updates before entry j+1's -- the reference's
+// per-column summation order.
+template <int G, int U, bool VALS, bool ORDERED, typename F>
+__device__ __forceinline__ int walk_row(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
+                                        int lane, unsigned gm, F visit) {
+  int acc = 0;  // sum of visit()'s return values (symbolic: new keys)
+  for (int64_t c0 = a0; c0 < a1; c0 += G) {
+    const int nc = static_cast<int>(min(static_cast<int64_t>(G), a1 - c0));
+    int64_t b0 = 0;
+    int len = 0;
+    double av = 0.0;
+    if (lane < nc) {
+      const int32_t k = A.col[c0 + lane];
+      if constexpr (VALS) av = A.val[c0 + lane];
+      b0 = B.rpt[k];
+      len = static_cast<int>(B.rpt[k + 1] - b0);
+    }
+    const int maxlen = group_max<G>(len, gm);
+    if (maxlen <= G) {
+      for (int j0 = 0; j0 < nc; j0 += U) {
+        int32_t kc[U];
+        double bv[U];
+        double aj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = min(j0 + u, G - 1);
+          const int64_t bj = __shfl_sync(gm, b0, j, G);
+          const int lj = __shfl_sync(gm, len, j, G);
+          aj[u] = VALS ? __shfl_sync(gm, av, j, G) : 0.0;
+          const bool ok = (j0 + u < nc) && lane < lj;
+          kc[u] = ok ? B.col[bj + lane] : -1;
+          if constexpr (VALS) bv[u] = ok ? B.val[bj + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (j0 + u < nc) {
+            if (kc[u] >= 0) acc += visit(kc[u], VALS ? __dmul_rn(aj[u], bv[u]) : 0.0);
+            if constexpr (ORDERED) __syncwarp(gm);
+          }
+        }
+      }
+    } else {
+      for (int j = 0; j < nc; ++j) {
+        const int64_t bj = __shfl_sync(gm, b0, j, G);
+        const int lj = __shfl_sync(gm, len, j, G);
+        const double a = VALS ? __shfl_sync(gm, av, j, G) : 0.0;
+        for (int q = lane; q < lj; q += G) {
+          const int32_t key = B.col[bj + q];
+          acc += visit(key, VALS ? __dmul_rn(a, B.val[bj + q]) : 0.0);
+        }
+        if constexpr (ORDERED) __syncwarp(gm);
+      }
+    }
+  }
+  return acc;
+}
+
 // --------------------------------------------------------- K6 symbolic
 // Group kernel: G lanes per output row, NGRP rows in flight per block, one
 // pow2 table of T int32 slots per row in shared memory. Persistent over the
 // bin's rows (grid = resident blocks). The A row is walked entry by entry and
 // the group's lanes stride the entry's B row.
+__device__ __forceinline__ int ceil_log2_ll(long long x) {  // x >= 1
+  return x <= 1 ? 0 : 64 - __clzll(x - 1);
+}
+
 template <int G, int T, int NGRP>
 __global__ void __launch_bounds__(G* NGRP)
     k_sym_group(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+  constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + (threadIdx.x / G) * T;
   const int lane = threadIdx.x % G;
@@ -489,17 +597,18 @@ __global__ void __launch_bounds__(G* NGRP)
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * NGRP + threadIdx.x / G; idx < rl.count;
        idx += stride) {
     const int64_t row = rl.row(idx);
-    if (rpt[row] == 0) continue;  // no products: nnz 0 (pipeline.cpp:368-371)
-#pragma unroll 4
-    for (int s = lane; s < T; s += G) tab[s] = -1;
+    const long long np = rpt[row];
+    if (np == 0) continue;  // no products: nnz 0 (pipeline.cpp:368-371)
+    // The row's table: 2*nprod slots (load <= 1/2), capped at T (> the bin's
+    // nprod bound, so it never fills).
+    const int lg = min(LOG_T, ceil_log2_ll(2 * np));
+    const int tsz = 1 << lg;
+    const Hash hs = make_hash(scale, lg);
+    for (int s = lane; s < tsz; s += G) tab[s] = -1;
     __syncwarp(gm);
-    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
-    int cnt = 0;
-    for (int64_t p = a0; p < a1; ++p) {
-      const int32_t k = A.col[p];
-      const int64_t b1 = B.rpt[k + 1];
-      for (int64_t q = B.rpt[k] + lane; q < b1; q += G) cnt += sym_insert(tab, B.col[q], scale, T - 1);
-    }
+    int cnt = walk_row<G, 8, false, false>(
+        A, B, A.rpt[row], A.rpt[row + 1], lane, gm,
+        [tab, hs](int32_t key, double) { return sym_insert(tab, key, hs); });
     cnt = group_sum<G>(cnt, gm);
     __syncwarp(gm);
     if (lane == 0) rpt[row] = cnt;
@@ -520,6 +629,7 @@ __global__ void __launch_bounds__(THREADS)
   __shared__ long long s_red[32];
   constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Hash hs = make_hash(scale, log2_const<T>());
   for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
     const int64_t row = rl.row(idx);
     if (rpt[row] == 0) continue;
@@ -536,7 +646,7 @@ __global__ void __launch_bounds__(THREADS)
       const int64_t b0 = B.rpt[k], b1 = B.rpt[k + 1];
       for (int64_t qb = b0; qb < b1; qb += 32) {
         const int64_t q = qb + lane;
-        const int nw = q < b1 ? sym_insert(tab, B.col[q], scale, T - 1) : 0;
+        const int nw = q < b1 ? sym_insert(tab, B.col[q], hs) : 0;
         if constexpr (SPILL) {
           const unsigned bal = __ballot_sync(kFull, nw);
           int abort = 0;
@@ -590,7 +700,9 @@ __global__ void __launch_bounds__(1024)
     long long t = 2;
     while (t < want) t <<= 1;
     if (t > slots_per_block) t = slots_per_block;
-    const uint32_t mask = static_cast<uint32_t>(t - 1);
+    int lg = 0;
+    while ((1ll << lg) < t) ++lg;
+    const Hash hs = make_hash(scale, lg);
     for (long long s = threadIdx.x; s < t; s += 1024) tab[s] = -1;
     __syncthreads();
     const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
@@ -598,7 +710,7 @@ __global__ void __launch_bounds__(1024)
     for (int64_t p = a0 + warp; p < a1; p += 32) {
       const int32_t k = A.col[p];
       const int64_t b1 = B.rpt[k + 1];
-      for (int64_t q = B.rpt[k] + lane; q < b1; q += 32) cnt += sym_insert(tab, B.col[q], scale, mask);
+      for (int64_t q = B.rpt[k] + lane; q < b1; q += 32) cnt += sym_insert(tab, B.col[q], hs);
     }
     const long long total = block_sum_ll<1024>(cnt, s_red);
     if (threadIdx.x == 0) rpt[row] = total;
@@ -606,9 +718,10 @@ __global__ void __launch_bounds__(1024)
 }
 
 // ---------------------------------------------------------- K7 numeric
-// Sort of (col << 32 | slot) keys held E per lane across a G-lane group.
-template <int G, int E>
-__device__ __forceinline__ void group_bitonic(unsigned long long (&v)[E], int lane, unsigned gm) {
+// Bitonic sort of N = G*E keys held E per lane (blocked layout: element
+// lane*E+i) across a G-lane group; ascending.
+template <int G, int E, typename K>
+__device__ __forceinline__ void group_bitonic(K (&v)[E], int lane, unsigned gm) {
   constexpr int N = G * E;
 #pragma unroll
   for (int k = 2; k <= N; k <<= 1) {
@@ -619,7 +732,7 @@ __device__ __forceinline__ void group_bitonic(unsigned long long (&v)[E], int la
 #pragma unroll
         for (int i = 0; i < E; ++i) {
           const int e = lane * E + i;
-          const unsigned long long other = __shfl_xor_sync(gm, v[i], lj, G);
+          const K other = __shfl_xor_sync(gm, v[i], lj, G);
           const bool up = (e & k) == 0;
           const bool lower = (e & j) == 0;
           v[i] = (lower == up) ? min(v[i], other) : max(v[i], other);
@@ -631,7 +744,7 @@ __device__ __forceinline__ void group_bitonic(unsigned long long (&v)[E], int la
           if (pi > i) {
             const int e = lane * E + i;
             const bool up = (e & k) == 0;
-            const unsigned long long a = v[i], b = v[pi];
+            const K a = v[i], b = v[pi];
             const bool sw = up ? (a > b) : (a < b);
             v[i] = sw ? b : a;
             v[pi] = sw ? a : b;
@@ -642,21 +755,46 @@ __device__ __forceinline__ void group_bitonic(unsigned long long (&v)[E], int la
   }
 }
 
+// Sorts the n condensed keys of buf (n <= G*E) in place, with the smallest
+// network that covers n.
+template <int G, int E, typename K>
+__device__ __forceinline__ void group_sort_inplace(K* buf, int n, int lane, unsigned gm) {
+  if constexpr (E > 1) {
+    if (n <= G * E / 2) {
+      group_sort_inplace<G, (E > 1 ? E / 2 : 1), K>(buf, n, lane, gm);
+      return;
+    }
+  }
+  K v[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int e = lane * E + i;
+    v[i] = e < n ? buf[e] : static_cast<K>(~static_cast<K>(0));
+  }
+  group_bitonic<G, E, K>(v, lane, gm);
+#pragma unroll
+  for (int i = 0; i < E; ++i) buf[lane * E + i] = v[i];
+}
+
 // Group kernel: G lanes per row; per group T key slots + T fp64 values +
-// G*E packed sort keys in shared memory. Ordered steps over the A row (see
-// the header comment), then condense (hash_tables.cpp:125-135), a group
-// bitonic sort by column, and the write of C(i,:) at rpt[i].
+// G*E sort keys in shared memory. Ordered steps over the A row (see the
+// header comment); then condense (hash_tables.cpp:125-135), a bitonic sort by
+// column (hash_tables.cpp:137-177) and a coalesced write of C(i,:) at rpt[i].
+// The sort key packs (col - min col) with the slot index into 32 bits when the
+// row's column span allows (64 bits otherwise).
 template <int G, int T, int E, int NGRP>
 __global__ void __launch_bounds__(G* NGRP)
     k_num_group(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
                 DevInfo* info) {
   constexpr int NMAX = G * E;
+  constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
   unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * (T * 12 + NMAX * 8);
   double* vals = reinterpret_cast<double*>(gbase);
   unsigned long long* packed = reinterpret_cast<unsigned long long*>(gbase + T * 8);
+  uint32_t* packed32 = reinterpret_cast<uint32_t*>(packed);
   int32_t* keys = reinterpret_cast<int32_t*>(gbase + T * 8 + NMAX * 8);
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
@@ -667,51 +805,69 @@ __global__ void __launch_bounds__(G* NGRP)
     const int64_t base = rpt[row];
     const int n = static_cast<int>(rpt[row + 1] - base);
     if (n == 0) continue;
-#pragma unroll 4
-    for (int s = lane; s < T; s += G) {
+    const int lg = min(LOG_T, ceil_log2_ll(2 * static_cast<long long>(n)));
+    const int tsz = 1 << lg;
+    const Hash hs = make_hash(scale, lg);
+    for (int s = lane; s < tsz; s += G) {
       keys[s] = -1;
       vals[s] = 0.0;
     }
     __syncwarp(gm);
-    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
-    for (int64_t p = a0; p < a1; ++p) {
-      const int32_t k = A.col[p];
-      const double av = A.val[p];
-      const int64_t b1 = B.rpt[k + 1];
-      for (int64_t q = B.rpt[k] + lane; q < b1; q += G) {
-        const double x = __dmul_rn(av, B.val[q]);
-        const uint32_t s = num_slot(keys, B.col[q], scale, T - 1);
-        vals[s] = __dadd_rn(vals[s], x);
-      }
-      __syncwarp(gm);
-    }
-    int run = 0;
-#pragma unroll 4
-    for (int s0 = 0; s0 < T; s0 += G) {
-      const int s = s0 + lane;
+    walk_row<G, 4, true, true>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm,
+                               [keys, vals, hs](int32_t key, double x) {
+                                 const uint32_t s = num_slot(keys, key, hs);
+                                 vals[s] = __dadd_rn(vals[s], x);
+                                 return 0;
+                               });
+    // column range of the row, for the 32-bit sort key
+    int kmin = 0x7fffffff, kmax = -1;
+    for (int s = lane; s < tsz; s += G) {
       const int32_t key = keys[s];
+      if (key != -1) {
+        kmin = min(kmin, key);
+        kmax = max(kmax, key);
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(gm, kmin, o, G));
+      kmax = max(kmax, __shfl_xor_sync(gm, kmax, o, G));
+    }
+    const bool narrow = static_cast<unsigned>(kmax - kmin) < ((0xffffffffu >> lg) - 1u);
+    int run = 0;
+    for (int s0 = 0; s0 < tsz; s0 += G) {
+      const int s = s0 + lane;
+      const int32_t key = s < tsz ? keys[s] : -1;
       const bool occ = key != -1;
       const unsigned bal = __ballot_sync(gm, occ) >> gshift;
-      if (occ)
-        packed[run + __popc(bal & ((1u << lane) - 1u))] =
-            (static_cast<unsigned long long>(static_cast<uint32_t>(key)) << 32) | static_cast<uint32_t>(s);
+      if (occ) {
+        const int at = run + __popc(bal & ((1u << lane) - 1u));
+        if (narrow)
+          packed32[at] = (static_cast<uint32_t>(key - kmin) << lg) | static_cast<uint32_t>(s);
+        else
+          packed[at] = (static_cast<unsigned long long>(static_cast<uint32_t>(key)) << 32) |
+                       static_cast<uint32_t>(s);
+      }
       run += __popc(bal);
     }
     if (run != n && lane == 0) atomicOr(&info->error, kErrNumericCount);
     __syncwarp(gm);
-    unsigned long long v[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int e = lane * E + i;
-      v[i] = e < n ? packed[e] : ~0ull;
-    }
-    group_bitonic<G, E>(v, lane, gm);
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int e = lane * E + i;
-      if (e < n) {
-        ccol[base + e] = static_cast<int32_t>(v[i] >> 32);
-        cval[base + e] = vals[static_cast<uint32_t>(v[i])];
+    if (narrow) {
+      group_sort_inplace<G, E, uint32_t>(packed32, n, lane, gm);
+      __syncwarp(gm);
+      const uint32_t smask = (1u << lg) - 1u;
+      for (int e = lane; e < n; e += G) {
+        const uint32_t v = packed32[e];
+        ccol[base + e] = kmin + static_cast<int32_t>(v >> lg);
+        cval[base + e] = vals[v & smask];
+      }
+    } else {
+      group_sort_inplace<G, E, unsigned long long>(packed, n, lane, gm);
+      __syncwarp(gm);
+      for (int e = lane; e < n; e += G) {
+        const unsigned long long v = packed[e];
+        ccol[base + e] = static_cast<int32_t>(v >> 32);
+        cval[base + e] = vals[static_cast<uint32_t>(v)];
       }
     }
     __syncwarp(gm);
@@ -751,6 +907,7 @@ __global__ void __launch_bounds__(THREADS)
   int32_t* keys = reinterpret_cast<int32_t*>(smem_raw + T * 8 + NMAX * 8);
   __shared__ long long s_red[32];
   constexpr int PER = T / THREADS;
+  const Hash hs = make_hash(scale, log2_const<T>());
   for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
     const int64_t row = rl.row(idx);
     const int64_t base = rpt[row];
@@ -768,7 +925,7 @@ __global__ void __launch_bounds__(THREADS)
       const int64_t b1 = B.rpt[k + 1];
       for (int64_t q = B.rpt[k] + threadIdx.x; q < b1; q += THREADS) {
         const double x = __dmul_rn(av, B.val[q]);
-        const uint32_t s = num_slot(keys, B.col[q], scale, T - 1);
+        const uint32_t s = num_slot(keys, B.col[q], hs);
         vals[s] = __dadd_rn(vals[s], x);
       }
       __syncthreads();
@@ -828,7 +985,9 @@ __global__ void __launch_bounds__(kGlobalThreads)
     int64_t t = 2;
     while (t < 2 * n) t <<= 1;
     if (t > slots_per_block) t = slots_per_block;
-    const uint32_t mask = static_cast<uint32_t>(t - 1);
+    int lg = 0;
+    while ((1ll << lg) < t) ++lg;
+    const Hash hs = make_hash(scale, lg);
     for (int64_t s = threadIdx.x; s < t; s += kGlobalThreads) {
       keys[s] = -1;
       vals[s] = 0.0;
@@ -845,7 +1004,7 @@ __global__ void __launch_bounds__(kGlobalThreads)
       const int64_t b1 = B.rpt[k + 1];
       for (int64_t q = B.rpt[k] + threadIdx.x; q < b1; q += kGlobalThreads) {
         const double x = __dmul_rn(av, B.val[q]);
-        const uint32_t s = num_slot(keys, B.col[q], scale, mask);
+        const uint32_t s = num_slot(keys, B.col[q], hs);
         vals[s] = __dadd_rn(vals[s], x);
       }
       __syncthreads();
