@@ -302,6 +302,7 @@ struct spgemm_pipeline {
   int64_t nrb = 0, ntiles = 0;
   uint32_t scale = 107;
   double avg_b_len = 0;
+  bool idx32 = true;
 
   int64_t* d_rpt = nullptr;
   unsigned char* d_arena = nullptr;
@@ -475,11 +476,15 @@ void spgemm_pipeline::symbolic_binning() {
 // Tier choice per bin from the preset's inclusive upper bound on nprod (the
 // bin invariant guarantees the table never fills). G (lanes per row) follows
 // the mean B row length so the lanes striding a B row stay busy.
+// Group kernels index B with 32-bit offsets when nnz(A), nnz(B) < 2^31.
+#define SYMG(G, T, N) (idx32 ? &k_sym_group<G, T, N, int32_t> : &k_sym_group<G, T, N, int64_t>)
+#define NUMG(G, T, E, N) (idx32 ? &k_num_group<G, T, E, N, int32_t> : &k_num_group<G, T, E, N, int64_t>)
+
 void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s) {
   const int64_t u = sym_plan.config.upper[bin];
   const bool g8 = avg_b_len <= 8.0;
   auto group = [&](auto kern, int G, int T, int NGRP) {
-    const size_t smem = static_cast<size_t>(NGRP) * T * 4;
+    const size_t smem = static_cast<size_t>(NGRP) * (T * 4 + G * 16);
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
     SPG_LAUNCH(ctx, "k_sym_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
@@ -510,17 +515,17 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     return;
   }
   if (u < 64) {
-    if (g8) group(k_sym_group<8, 64, 32>, 8, 64, 32);
-    else group(k_sym_group<32, 64, 8>, 32, 64, 8);
+    if (g8) group(SYMG(8, 64, 32), 8, 64, 32);
+    else group(SYMG(32, 64, 8), 32, 64, 8);
   } else if (u < 512) {
-    if (g8) group(k_sym_group<8, 512, 32>, 8, 512, 32);
-    else group(k_sym_group<32, 512, 8>, 32, 512, 8);
+    if (g8) group(SYMG(8, 512, 32), 8, 512, 32);
+    else group(SYMG(32, 512, 8), 32, 512, 8);
   } else if (u < 1024) {
-    if (g8) group(k_sym_group<8, 1024, 16>, 8, 1024, 16);
-    else group(k_sym_group<32, 1024, 8>, 32, 1024, 8);
+    if (g8) group(SYMG(8, 1024, 16), 8, 1024, 16);
+    else group(SYMG(32, 1024, 8), 32, 1024, 8);
   } else if (u < 2048) {
-    if (g8) group(k_sym_group<8, 2048, 8>, 8, 2048, 8);
-    else group(k_sym_group<32, 2048, 8>, 32, 2048, 8);
+    if (g8) group(SYMG(8, 2048, 8), 8, 2048, 8);
+    else group(SYMG(32, 2048, 8), 32, 2048, 8);
   } else if (u < 4096) {
     block(k_sym_block<4096, 256, false>, 4096, 256);
   } else if (u < 8192) {
@@ -629,7 +634,7 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
   const int64_t u = num_plan.config.upper[bin];
   const bool g8 = avg_b_len <= 8.0;
   auto group = [&](auto kern, int G, int T, int E, int NGRP) {
-    const size_t smem = static_cast<size_t>(NGRP) * (T * 12 + G * E * 8);
+    const size_t smem = static_cast<size_t>(NGRP) * (T * 12 + G * E * 8 + G * 16);
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
     SPG_LAUNCH(ctx, "k_num_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
@@ -647,15 +652,15 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
                k_num_global<<<gblocks, kGlobalThreads, 0, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, gkeys,
                                                     gvals, gbits, gslots, gwords, d_info_num));
   } else if (u <= 32) {
-    if (g8) group(k_num_group<8, 64, 4, 32>, 8, 64, 4, 32);
-    else group(k_num_group<32, 64, 1, 8>, 32, 64, 1, 8);
+    if (g8) group(NUMG(8, 64, 4, 32), 8, 64, 4, 32);
+    else group(NUMG(32, 64, 1, 8), 32, 64, 1, 8);
   } else if (u <= 128) {
-    if (g8) group(k_num_group<8, 256, 16, 16>, 8, 256, 16, 16);
-    else group(k_num_group<32, 256, 4, 8>, 32, 256, 4, 8);
+    if (g8) group(NUMG(8, 256, 16, 16), 8, 256, 16, 16);
+    else group(NUMG(32, 256, 4, 8), 32, 256, 4, 8);
   } else if (u <= 256) {
-    group(k_num_group<32, 512, 8, 8>, 32, 512, 8, 8);
+    group(NUMG(32, 512, 8, 8), 32, 512, 8, 8);
   } else if (u <= 512) {
-    group(k_num_group<32, 1024, 16, 4>, 32, 1024, 16, 4);
+    group(NUMG(32, 1024, 16, 4), 32, 1024, 16, 4);
   } else if (u <= 1024) {
     block(k_num_block<2048, 256, 1024>, 2048, 256, 1024);
   } else if (u <= 2048) {
@@ -953,6 +958,7 @@ spgemm_status spgemm_pipeline_create(spgemm_ctx* ctx, const spgemm_csr_view* a,
         stage_input(ctx, b, &p->B, p->owned + 3, &p->b_nnz);
       }
       p->M = a->rows;
+      p->idx32 = p->a_nnz < (int64_t(1) << 31) && p->b_nnz < (int64_t(1) << 31);
       p->avg_b_len = b->rows > 0 ? static_cast<double>(p->b_nnz) / static_cast<double>(b->rows) : 0;
       for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     } catch (...) {

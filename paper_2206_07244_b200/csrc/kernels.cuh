@@ -146,10 +146,9 @@ __host__ __device__ constexpr int log2_const() {
 }
 
 template <typename Slot>
-__device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, const Hash& hs) {
-  uint32_t h = hs.home(key) & hs.mask;
+__device__ __forceinline__ int sym_insert_slow(Slot* tab, int32_t key, const Hash& hs, uint32_t h,
+                                            int32_t cur) {
   while (true) {
-    int32_t cur = *reinterpret_cast<volatile int32_t*>(tab + h);
     if (cur == key) return 0;
     if (cur == -1) {
       cur = atomicCAS(reinterpret_cast<int*>(tab + h), -1, key);
@@ -157,20 +156,38 @@ __device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, const Hash& hs
       if (cur == key) return 0;
     }
     h = (h + 1) & hs.mask;
+    cur = *reinterpret_cast<volatile int32_t*>(tab + h);
   }
 }
 
-__device__ __forceinline__ uint32_t num_slot(int32_t* keys, int32_t key, const Hash& hs) {
-  uint32_t h = hs.home(key) & hs.mask;
+// Common case first: one read of the home slot; only a miss (empty slot to
+// claim, or a collision) leaves the straight-line path.
+template <typename Slot>
+__device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, const Hash& hs) {
+  const uint32_t h = hs.home(key) & hs.mask;
+  const int32_t cur = *reinterpret_cast<volatile int32_t*>(tab + h);
+  if (cur == key) return 0;
+  return sym_insert_slow(tab, key, hs, h, cur);
+}
+
+__device__ __forceinline__ uint32_t num_slot_slow(int32_t* keys, int32_t key, const Hash& hs, uint32_t h,
+                                               int32_t cur) {
   while (true) {
-    int32_t cur = *reinterpret_cast<volatile int32_t*>(keys + h);
     if (cur == key) return h;
     if (cur == -1) {
       cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, key);
       if (cur == -1 || cur == key) return h;
     }
     h = (h + 1) & hs.mask;
+    cur = *reinterpret_cast<volatile int32_t*>(keys + h);
   }
+}
+
+__device__ __forceinline__ uint32_t num_slot(int32_t* keys, int32_t key, const Hash& hs) {
+  const uint32_t h = hs.home(key) & hs.mask;
+  const int32_t cur = *reinterpret_cast<volatile int32_t*>(keys + h);
+  if (cur == key) return h;
+  return num_slot_slow(keys, key, hs, h, cur);
 }
 
 // --------------------------------------------------- block-level helpers
@@ -521,36 +538,46 @@ __device__ __forceinline__ int group_max(int v, unsigned gm) {
 // within an entry the B columns are distinct (no two lanes share a slot), and
 // the barrier orders entry j's updates before entry j+1's -- the reference's
 // per-column summation order.
-template <int G, int U, bool VALS, bool ORDERED, typename F>
+// Per-entry metadata of one A-row chunk, staged in shared memory so each step
+// reads it with one broadcast 16-byte load.
+struct EntryMeta {
+  int32_t b0;   // B row start (32-bit index path)
+  int32_t len;  // B row length
+  double av;    // A value
+};
+
+template <int G, int U, bool VALS, bool ORDERED, typename IT, typename F>
 __device__ __forceinline__ int walk_row(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
-                                        int lane, unsigned gm, F visit) {
+                                        int lane, unsigned gm, EntryMeta* meta, F visit) {
   int acc = 0;  // sum of visit()'s return values (symbolic: new keys)
   for (int64_t c0 = a0; c0 < a1; c0 += G) {
     const int nc = static_cast<int>(min(static_cast<int64_t>(G), a1 - c0));
-    int64_t b0 = 0;
+    IT b0 = 0;
     int len = 0;
     double av = 0.0;
     if (lane < nc) {
       const int32_t k = A.col[c0 + lane];
       if constexpr (VALS) av = A.val[c0 + lane];
-      b0 = B.rpt[k];
-      len = static_cast<int>(B.rpt[k + 1] - b0);
+      const int64_t r0 = B.rpt[k];
+      b0 = static_cast<IT>(r0);
+      len = static_cast<int>(B.rpt[k + 1] - r0);
     }
     const int maxlen = group_max<G>(len, gm);
-    if (maxlen <= G) {
+    if (sizeof(IT) == 4 && maxlen <= G) {
+      if (lane < nc) meta[lane] = EntryMeta{static_cast<int32_t>(b0), len, av};
+      __syncwarp(gm);
       for (int j0 = 0; j0 < nc; j0 += U) {
         int32_t kc[U];
         double bv[U];
         double aj[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int j = min(j0 + u, G - 1);
-          const int64_t bj = __shfl_sync(gm, b0, j, G);
-          const int lj = __shfl_sync(gm, len, j, G);
-          aj[u] = VALS ? __shfl_sync(gm, av, j, G) : 0.0;
-          const bool ok = (j0 + u < nc) && lane < lj;
-          kc[u] = ok ? B.col[bj + lane] : -1;
-          if constexpr (VALS) bv[u] = ok ? B.val[bj + lane] : 0.0;
+          const EntryMeta m = meta[min(j0 + u, G - 1)];
+          aj[u] = m.av;
+          const bool ok = (j0 + u < nc) && lane < m.len;
+          const int at = m.b0 + lane;
+          kc[u] = ok ? B.col[at] : -1;
+          if constexpr (VALS) bv[u] = ok ? B.val[at] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -560,9 +587,10 @@ __device__ __forceinline__ int walk_row(const DevCsr& A, const DevCsr& B, int64_
           }
         }
       }
+      __syncwarp(gm);
     } else {
       for (int j = 0; j < nc; ++j) {
-        const int64_t bj = __shfl_sync(gm, b0, j, G);
+        const IT bj = __shfl_sync(gm, b0, j, G);
         const int lj = __shfl_sync(gm, len, j, G);
         const double a = VALS ? __shfl_sync(gm, av, j, G) : 0.0;
         for (int q = lane; q < lj; q += G) {
@@ -576,6 +604,23 @@ __device__ __forceinline__ int walk_row(const DevCsr& A, const DevCsr& B, int64_
   return acc;
 }
 
+// Fills n (multiple of 4 or not) int32 slots with -1 using 16-byte stores.
+template <int G>
+__device__ __forceinline__ void fill_empty(int32_t* tab, int n, int lane) {
+  int4* t4 = reinterpret_cast<int4*>(tab);
+  const int n4 = n >> 2;
+  for (int s = lane; s < n4; s += G) t4[s] = make_int4(-1, -1, -1, -1);
+  for (int s = (n4 << 2) + lane; s < n; s += G) tab[s] = -1;
+}
+
+template <int G>
+__device__ __forceinline__ void fill_zero(double* v, int n, int lane) {
+  double2* v2 = reinterpret_cast<double2*>(v);
+  const int n2 = n >> 1;
+  for (int s = lane; s < n2; s += G) v2[s] = make_double2(0.0, 0.0);
+  if ((n & 1) && lane == 0) v[n - 1] = 0.0;
+}
+
 // --------------------------------------------------------- K6 symbolic
 // Group kernel: G lanes per output row, NGRP rows in flight per block, one
 // pow2 table of T int32 slots per row in shared memory. Persistent over the
@@ -585,12 +630,14 @@ __device__ __forceinline__ int ceil_log2_ll(long long x) {  // x >= 1
   return x <= 1 ? 0 : 64 - __clzll(x - 1);
 }
 
-template <int G, int T, int NGRP>
+template <int G, int T, int NGRP, typename IT>
 __global__ void __launch_bounds__(G* NGRP)
     k_sym_group(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + (threadIdx.x / G) * T;
+  EntryMeta* meta = reinterpret_cast<EntryMeta*>(smem_raw + static_cast<size_t>(NGRP) * T * 4) +
+                    (threadIdx.x / G) * G;
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NGRP;
@@ -604,10 +651,10 @@ __global__ void __launch_bounds__(G* NGRP)
     const int lg = min(LOG_T, ceil_log2_ll(2 * np));
     const int tsz = 1 << lg;
     const Hash hs = make_hash(scale, lg);
-    for (int s = lane; s < tsz; s += G) tab[s] = -1;
+    fill_empty<G>(tab, tsz, lane);
     __syncwarp(gm);
-    int cnt = walk_row<G, 8, false, false>(
-        A, B, A.rpt[row], A.rpt[row + 1], lane, gm,
+    int cnt = walk_row<G, 8, false, false, IT>(
+        A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
         [tab, hs](int32_t key, double) { return sym_insert(tab, key, hs); });
     cnt = group_sum<G>(cnt, gm);
     __syncwarp(gm);
@@ -782,7 +829,7 @@ __device__ __forceinline__ void group_sort_inplace(K* buf, int n, int lane, unsi
 // column (hash_tables.cpp:137-177) and a coalesced write of C(i,:) at rpt[i].
 // The sort key packs (col - min col) with the slot index into 32 bits when the
 // row's column span allows (64 bits otherwise).
-template <int G, int T, int E, int NGRP>
+template <int G, int T, int E, int NGRP, typename IT>
 __global__ void __launch_bounds__(G* NGRP)
     k_num_group(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
@@ -791,7 +838,8 @@ __global__ void __launch_bounds__(G* NGRP)
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
-  unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * (T * 12 + NMAX * 8);
+  unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * (T * 12 + NMAX * 8 + G * 16);
+  EntryMeta* meta = reinterpret_cast<EntryMeta*>(gbase + T * 12 + NMAX * 8);
   double* vals = reinterpret_cast<double*>(gbase);
   unsigned long long* packed = reinterpret_cast<unsigned long long*>(gbase + T * 8);
   uint32_t* packed32 = reinterpret_cast<uint32_t*>(packed);
@@ -808,12 +856,10 @@ __global__ void __launch_bounds__(G* NGRP)
     const int lg = min(LOG_T, ceil_log2_ll(2 * static_cast<long long>(n)));
     const int tsz = 1 << lg;
     const Hash hs = make_hash(scale, lg);
-    for (int s = lane; s < tsz; s += G) {
-      keys[s] = -1;
-      vals[s] = 0.0;
-    }
+    fill_empty<G>(keys, tsz, lane);
+    fill_zero<G>(vals, tsz, lane);
     __syncwarp(gm);
-    walk_row<G, 4, true, true>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm,
+    walk_row<G, 4, true, true, IT>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
                                [keys, vals, hs](int32_t key, double x) {
                                  const uint32_t s = num_slot(keys, key, hs);
                                  vals[s] = __dadd_rn(vals[s], x);
