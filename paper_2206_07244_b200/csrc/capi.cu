@@ -477,14 +477,14 @@ void spgemm_pipeline::symbolic_binning() {
 // bin invariant guarantees the table never fills). G (lanes per row) follows
 // the mean B row length so the lanes striding a B row stay busy.
 // Group kernels index B with 32-bit offsets when nnz(A), nnz(B) < 2^31.
-#define SYMG(G, T, N) (idx32 ? &k_sym_group<G, T, N, int32_t> : &k_sym_group<G, T, N, int64_t>)
+#define SYMG(G, T, N, WB) (idx32 ? &k_sym_group<G, T, N, int32_t, WB> : &k_sym_group<G, T, N, int64_t, WB>)
 #define NUMG(G, T, E, N) (idx32 ? &k_num_group<G, T, E, N, int32_t> : &k_num_group<G, T, E, N, int64_t>)
 
 void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s) {
   const int64_t u = sym_plan.config.upper[bin];
   const bool g8 = avg_b_len <= 8.0;
-  auto group = [&](auto kern, int G, int T, int NGRP) {
-    const size_t smem = static_cast<size_t>(NGRP) * (T * 4 + G * 16);
+  auto group = [&](auto kern, int G, int T, int NGRP, int WB) {
+    const size_t smem = static_cast<size_t>(NGRP) * (static_cast<size_t>(std::max(T, WB)) * 4 + G * 16);
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
     SPG_LAUNCH(ctx, "k_sym_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
@@ -514,18 +514,19 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     dev_free(pool, s);
     return;
   }
+  // group kernels: (G, T, groups per block, bitmap words per group)
   if (u < 64) {
-    if (g8) group(SYMG(8, 64, 32), 8, 64, 32);
-    else group(SYMG(32, 64, 8), 32, 64, 8);
+    if (g8) group(SYMG(8, 64, 32, 256), 8, 64, 32, 256);
+    else group(SYMG(32, 64, 8, 256), 32, 64, 8, 256);
   } else if (u < 512) {
-    if (g8) group(SYMG(8, 512, 32), 8, 512, 32);
-    else group(SYMG(32, 512, 8), 32, 512, 8);
+    if (g8) group(SYMG(8, 512, 32, 512), 8, 512, 32, 512);
+    else group(SYMG(32, 512, 8, 512), 32, 512, 8, 512);
   } else if (u < 1024) {
-    if (g8) group(SYMG(8, 1024, 16), 8, 1024, 16);
-    else group(SYMG(32, 1024, 8), 32, 1024, 8);
+    if (g8) group(SYMG(8, 1024, 16, 1024), 8, 1024, 16, 1024);
+    else group(SYMG(32, 1024, 8, 1024), 32, 1024, 8, 1024);
   } else if (u < 2048) {
-    if (g8) group(SYMG(8, 2048, 8), 8, 2048, 8);
-    else group(SYMG(32, 2048, 8), 32, 2048, 8);
+    if (g8) group(SYMG(8, 2048, 8, 2048), 8, 2048, 8, 2048);
+    else group(SYMG(32, 2048, 8, 2048), 32, 2048, 8, 2048);
   } else if (u < 4096) {
     block(k_sym_block<4096, 256, false>, 4096, 256);
   } else if (u < 8192) {
@@ -634,7 +635,7 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
   const int64_t u = num_plan.config.upper[bin];
   const bool g8 = avg_b_len <= 8.0;
   auto group = [&](auto kern, int G, int T, int E, int NGRP) {
-    const size_t smem = static_cast<size_t>(NGRP) * (T * 12 + G * E * 8 + G * 16);
+    const size_t smem = static_cast<size_t>(NGRP) * ((T + 2) * 8 + G * E * 8 + T * 4 + G * 16);
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
     SPG_LAUNCH(ctx, "k_num_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,

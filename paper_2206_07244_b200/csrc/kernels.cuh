@@ -190,6 +190,40 @@ __device__ __forceinline__ uint32_t num_slot(int32_t* keys, int32_t key, const H
   return num_slot_slow(keys, key, hs, h, cur);
 }
 
+// Batched lookups: the V first-probe reads are issued back to back (a plain
+// read is safe: an occupied slot never changes), and only misses take the
+// probing loop. Invalid entries (key < 0) count as hits.
+template <int V>
+__device__ __forceinline__ int sym_insert_batch(int32_t* tab, const int32_t (&key)[V], const Hash& hs) {
+  uint32_t h[V];
+  int32_t cur[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) h[v] = hs.home(key[v]) & hs.mask;
+#pragma unroll
+  for (int v = 0; v < V; ++v) cur[v] = key[v] >= 0 ? tab[h[v]] : key[v];
+  int n = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    if (cur[v] != key[v]) n += sym_insert_slow(tab, key[v], hs, h[v], cur[v]);
+  return n;
+}
+
+// Slot of each key (claimed if new); invalid entries (key < 0) get `dummy`.
+template <int V>
+__device__ __forceinline__ void num_slot_batch(int32_t* keys, const int32_t (&key)[V], const Hash& hs,
+                                               uint32_t dummy, uint32_t (&slot)[V]) {
+  int32_t cur[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) slot[v] = hs.home(key[v]) & hs.mask;
+#pragma unroll
+  for (int v = 0; v < V; ++v) cur[v] = key[v] >= 0 ? keys[slot[v]] : key[v];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    if (key[v] < 0) slot[v] = dummy;
+    else if (cur[v] != key[v]) slot[v] = num_slot_slow(keys, key[v], hs, slot[v], cur[v]);
+  }
+}
+
 // --------------------------------------------------- block-level helpers
 template <int THREADS>
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
@@ -604,6 +638,163 @@ __device__ __forceinline__ int walk_row(const DevCsr& A, const DevCsr& B, int64_
   return acc;
 }
 
+// Ordered walker for the numeric phase, 32-bit index path. As walk_row, but
+// the U steps' slot lookups/claims are batched (order-independent), then the
+// U value updates run in step order with a group barrier between them; lanes
+// without a product add 0.0 into a dummy slot so the update is branch-free.
+template <int G, int U>
+__device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
+                                             int lane, unsigned gm, EntryMeta* meta, int32_t* keys,
+                                             double* vals, const Hash& hs, uint32_t dummy) {
+  for (int64_t c0 = a0; c0 < a1; c0 += G) {
+    const int nc = static_cast<int>(min(static_cast<int64_t>(G), a1 - c0));
+    int len = 0;
+    if (lane < nc) {
+      const int32_t k = A.col[c0 + lane];
+      const double av = A.val[c0 + lane];
+      const int64_t r0 = B.rpt[k];
+      len = static_cast<int>(B.rpt[k + 1] - r0);
+      meta[lane] = EntryMeta{static_cast<int32_t>(r0), len, av};
+    }
+    const int maxlen = group_max<G>(len, gm);
+    __syncwarp(gm);
+    if (maxlen <= G) {
+      for (int j0 = 0; j0 < nc; j0 += U) {
+        int32_t kc[U];
+        double x[U];
+        uint32_t slot[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const EntryMeta m = meta[min(j0 + u, G - 1)];
+          const bool ok = (j0 + u < nc) && lane < m.len;
+          const int at = m.b0 + lane;
+          kc[u] = ok ? B.col[at] : -1;
+          x[u] = ok ? __dmul_rn(m.av, B.val[at]) : 0.0;
+        }
+        num_slot_batch<U>(keys, kc, hs, dummy, slot);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (j0 + u < nc) {
+            vals[slot[u]] = __dadd_rn(vals[slot[u]], x[u]);
+            __syncwarp(gm);
+          }
+        }
+      }
+    } else {
+      for (int j = 0; j < nc; ++j) {
+        const EntryMeta m = meta[j];
+        for (int qb = 0; qb < m.len; qb += G) {
+          const int q = qb + lane;
+          int32_t kc[1] = {q < m.len ? B.col[m.b0 + q] : -1};
+          const double xv = q < m.len ? __dmul_rn(m.av, B.val[m.b0 + q]) : 0.0;
+          uint32_t slot[1];
+          num_slot_batch<1>(keys, kc, hs, dummy, slot);
+          vals[slot[0]] = __dadd_rn(vals[slot[0]], xv);
+        }
+        __syncwarp(gm);
+      }
+    }
+    __syncwarp(gm);
+  }
+}
+
+// Unordered walk of ONE staged chunk (the symbolic phase has no summation
+// order to keep): a step covers R = G/S A entries at once, S lanes per entry,
+// V products per lane (lane sl of a sub-group takes B(k, qb + sl + S*v), v < V:
+// coalesced within the sub-group). S is the smallest power of two with
+// S*V >= the chunk's longest B row (capped at G; longer rows loop). Per-step
+// bookkeeping is paid once per R*S*V products and each lane has V independent
+// inserts in flight. visit(keys[V]) gets -1 for empty positions.
+template <int G, int V, typename F>
+__device__ __forceinline__ int walk_chunk_multi(const DevCsr& B, int nc, int maxlen, int lane,
+                                                const EntryMeta* meta, F visit) {
+  int acc = 0;
+  int lgS = 0;
+  while ((1 << lgS) * V < maxlen && (1 << lgS) < G) ++lgS;
+  const int S = 1 << lgS;
+  const int R = G >> lgS;
+  const int sub = lane >> lgS, sl = lane & (S - 1);
+  for (int j0 = 0; j0 < nc; j0 += R) {
+    const int j = j0 + sub;
+    const EntryMeta m = meta[min(j, G - 1)];
+    const int lj = j < nc ? m.len : 0;
+    for (int qb = 0; qb < lj; qb += S * V) {
+      int32_t kc[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int q = qb + sl + S * v;
+        kc[v] = q < lj ? B.col[m.b0 + q] : -1;
+      }
+      acc += visit(kc);
+    }
+  }
+  return acc;
+}
+
+// Stages one chunk of up to G A entries (B row start/length, A value) in
+// shared memory; returns the chunk's longest B row. With SPAN, also reduces the
+// chunk's column range [lo, hi] (first/last column of each B row).
+template <int G, bool SPAN>
+__device__ __forceinline__ int stage_chunk(const DevCsr& A, const DevCsr& B, int64_t c0, int nc, int lane,
+                                           unsigned gm, EntryMeta* meta, bool vals, int32_t* lo,
+                                           int32_t* hi) {
+  int len = 0;
+  int32_t first = 0x7fffffff, last = -1;
+  if (lane < nc) {
+    const int32_t k = A.col[c0 + lane];
+    const double av = vals ? A.val[c0 + lane] : 0.0;
+    const int64_t r0 = B.rpt[k];
+    len = static_cast<int>(B.rpt[k + 1] - r0);
+    meta[lane] = EntryMeta{static_cast<int32_t>(r0), len, av};
+    if (SPAN && len > 0) {
+      first = B.col[r0];
+      last = B.col[r0 + len - 1];
+    }
+  }
+  if constexpr (SPAN) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      first = min(first, __shfl_xor_sync(gm, first, o, G));
+      last = max(last, __shfl_xor_sync(gm, last, o, G));
+    }
+    *lo = first;
+    *hi = last;
+  }
+  const int maxlen = group_max<G>(len, gm);
+  __syncwarp(gm);
+  return maxlen;
+}
+
+template <int G, int V, typename F>
+__device__ __forceinline__ int walk_row_multi(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
+                                              int lane, unsigned gm, EntryMeta* meta, F visit) {
+  int acc = 0;
+  for (int64_t c0 = a0; c0 < a1; c0 += G) {
+    const int nc = static_cast<int>(min(static_cast<int64_t>(G), a1 - c0));
+    const int maxlen = stage_chunk<G, false>(A, B, c0, nc, lane, gm, meta, false, nullptr, nullptr);
+    acc += walk_chunk_multi<G, V>(B, nc, maxlen, lane, meta, visit);
+    __syncwarp(gm);
+  }
+  return acc;
+}
+
+// Window bitmap insert: one bit per column of the row's column range; a set
+// returns whether the bit was new. Shared atomicOr runs at LDS throughput on
+// sm_100 (tools/micro/smem_atomics.cu), and there is no probing.
+template <int V>
+__device__ __forceinline__ int bm_insert_batch(uint32_t* bm, const int32_t (&key)[V], int32_t lo) {
+  int n = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    if (key[v] >= 0) {
+      const uint32_t off = static_cast<uint32_t>(key[v] - lo);
+      const uint32_t bit = 1u << (off & 31u);
+      n += (atomicOr(bm + (off >> 5), bit) & bit) == 0u;
+    }
+  }
+  return n;
+}
+
 // Fills n (multiple of 4 or not) int32 slots with -1 using 16-byte stores.
 template <int G>
 __device__ __forceinline__ void fill_empty(int32_t* tab, int n, int lane) {
@@ -611,6 +802,14 @@ __device__ __forceinline__ void fill_empty(int32_t* tab, int n, int lane) {
   const int n4 = n >> 2;
   for (int s = lane; s < n4; s += G) t4[s] = make_int4(-1, -1, -1, -1);
   for (int s = (n4 << 2) + lane; s < n; s += G) tab[s] = -1;
+}
+
+template <int G>
+__device__ __forceinline__ void fill_zero_words(uint32_t* w, int n, int lane) {
+  uint4* w4 = reinterpret_cast<uint4*>(w);
+  const int n4 = n >> 2;
+  for (int s = lane; s < n4; s += G) w4[s] = make_uint4(0u, 0u, 0u, 0u);
+  for (int s = (n4 << 2) + lane; s < n; s += G) w[s] = 0u;
 }
 
 template <int G>
@@ -630,13 +829,18 @@ __device__ __forceinline__ int ceil_log2_ll(long long x) {  // x >= 1
   return x <= 1 ? 0 : 64 - __clzll(x - 1);
 }
 
-template <int G, int T, int NGRP, typename IT>
+// Symbolic group kernel. Per group: WB words of shared memory (>= T) used
+// either as the row's window bitmap -- when the row is one chunk (<= G A
+// entries) and its column span fits WB*32 bits -- or as its hash table
+// (2*nprod slots, capped at T > the bin's nprod bound, so it never fills).
+template <int G, int T, int NGRP, typename IT, int WB>
 __global__ void __launch_bounds__(G* NGRP)
     k_sym_group(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+  static_assert(WB >= T, "bitmap region doubles as the hash table");
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + (threadIdx.x / G) * T;
-  EntryMeta* meta = reinterpret_cast<EntryMeta*>(smem_raw + static_cast<size_t>(NGRP) * T * 4) +
+  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + (threadIdx.x / G) * WB;
+  EntryMeta* meta = reinterpret_cast<EntryMeta*>(smem_raw + static_cast<size_t>(NGRP) * WB * 4) +
                     (threadIdx.x / G) * G;
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
@@ -646,16 +850,45 @@ __global__ void __launch_bounds__(G* NGRP)
     const int64_t row = rl.row(idx);
     const long long np = rpt[row];
     if (np == 0) continue;  // no products: nnz 0 (pipeline.cpp:368-371)
-    // The row's table: 2*nprod slots (load <= 1/2), capped at T (> the bin's
-    // nprod bound, so it never fills).
-    const int lg = min(LOG_T, ceil_log2_ll(2 * np));
-    const int tsz = 1 << lg;
-    const Hash hs = make_hash(scale, lg);
-    fill_empty<G>(tab, tsz, lane);
-    __syncwarp(gm);
-    int cnt = walk_row<G, 8, false, false, IT>(
-        A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
-        [tab, hs](int32_t key, double) { return sym_insert(tab, key, hs); });
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    int cnt = 0;
+    bool done = false;
+    if constexpr (sizeof(IT) == 4) {
+      if (a1 - a0 <= G) {
+        const int nc = static_cast<int>(a1 - a0);
+        int32_t lo, hi;
+        const int maxlen = stage_chunk<G, true>(A, B, a0, nc, lane, gm, meta, false, &lo, &hi);
+        const int64_t span = static_cast<int64_t>(hi) - lo + 1;
+        if (span <= static_cast<int64_t>(WB) * 32) {
+          const int words = static_cast<int>((span + 31) >> 5);
+          uint32_t* bm = reinterpret_cast<uint32_t*>(tab);
+          fill_zero_words<G>(bm, words, lane);
+          __syncwarp(gm);
+          cnt = walk_chunk_multi<G, 4>(B, nc, maxlen, lane, meta,
+                                       [bm, lo](const int32_t(&k)[4]) { return bm_insert_batch<4>(bm, k, lo); });
+        } else {
+          const int lg = min(LOG_T, ceil_log2_ll(2 * np));
+          const Hash hs = make_hash(scale, lg);
+          fill_empty<G>(tab, 1 << lg, lane);
+          __syncwarp(gm);
+          cnt = walk_chunk_multi<G, 4>(B, nc, maxlen, lane, meta,
+                                       [tab, hs](const int32_t(&k)[4]) { return sym_insert_batch<4>(tab, k, hs); });
+        }
+        done = true;
+      }
+    }
+    if (!done) {
+      const int lg = min(LOG_T, ceil_log2_ll(2 * np));
+      const Hash hs = make_hash(scale, lg);
+      fill_empty<G>(tab, 1 << lg, lane);
+      __syncwarp(gm);
+      if constexpr (sizeof(IT) == 4)
+        cnt = walk_row_multi<G, 4>(A, B, a0, a1, lane, gm, meta,
+                                   [tab, hs](const int32_t(&k)[4]) { return sym_insert_batch<4>(tab, k, hs); });
+      else
+        cnt = walk_row<G, 8, false, false, IT>(A, B, a0, a1, lane, gm, meta,
+                                               [tab, hs](int32_t key, double) { return sym_insert(tab, key, hs); });
+    }
     cnt = group_sum<G>(cnt, gm);
     __syncwarp(gm);
     if (lane == 0) rpt[row] = cnt;
@@ -838,12 +1071,14 @@ __global__ void __launch_bounds__(G* NGRP)
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
-  unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * (T * 12 + NMAX * 8 + G * 16);
-  EntryMeta* meta = reinterpret_cast<EntryMeta*>(gbase + T * 12 + NMAX * 8);
+  // per group: vals[T + 2] (slot T is the dummy), packed[NMAX], keys[T], meta[G]
+  constexpr size_t kGroupBytes = (T + 2) * 8 + NMAX * 8 + T * 4 + G * 16;
+  unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * kGroupBytes;
   double* vals = reinterpret_cast<double*>(gbase);
-  unsigned long long* packed = reinterpret_cast<unsigned long long*>(gbase + T * 8);
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(gbase + (T + 2) * 8);
   uint32_t* packed32 = reinterpret_cast<uint32_t*>(packed);
-  int32_t* keys = reinterpret_cast<int32_t*>(gbase + T * 8 + NMAX * 8);
+  int32_t* keys = reinterpret_cast<int32_t*>(gbase + (T + 2) * 8 + NMAX * 8);
+  EntryMeta* meta = reinterpret_cast<EntryMeta*>(gbase + (T + 2) * 8 + NMAX * 8 + T * 4);
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const unsigned gshift = (threadIdx.x & 31u) & ~(G - 1u);
@@ -859,12 +1094,17 @@ __global__ void __launch_bounds__(G* NGRP)
     fill_empty<G>(keys, tsz, lane);
     fill_zero<G>(vals, tsz, lane);
     __syncwarp(gm);
-    walk_row<G, 4, true, true, IT>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
-                               [keys, vals, hs](int32_t key, double x) {
-                                 const uint32_t s = num_slot(keys, key, hs);
-                                 vals[s] = __dadd_rn(vals[s], x);
-                                 return 0;
-                               });
+    if constexpr (sizeof(IT) == 4) {
+      walk_row_num<G, 4>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta, keys, vals, hs,
+                         static_cast<uint32_t>(T));
+    } else {
+      walk_row<G, 4, true, true, IT>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
+                                     [keys, vals, hs](int32_t key, double x) {
+                                       const uint32_t s = num_slot(keys, key, hs);
+                                       vals[s] = __dadd_rn(vals[s], x);
+                                       return 0;
+                                     });
+    }
     // column range of the row, for the 32-bit sort key
     int kmin = 0x7fffffff, kmax = -1;
     for (int s = lane; s < tsz; s += G) {
