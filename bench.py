@@ -155,18 +155,6 @@ def stencil_weak(n_ranks):
     return S._stencil((128, 128, 128 * n_ranks), offs, 26.0, -1.0)
 
 
-def nprod_split(nprod, parts):
-    """Contiguous row blocks balanced by the nprod prefix sum:
-    rank g takes rows whose exclusive prefix lies in [g*T/G, (g+1)*T/G)."""
-    pref = np.concatenate([[0], np.cumsum(nprod)])
-    total = pref[-1]
-    bounds = [0]
-    for g in range(1, parts):
-        bounds.append(int(np.searchsorted(pref[:-1], g * total / parts, side="left")))
-    bounds.append(len(nprod))
-    return bounds
-
-
 # ---------------------------------------------------------------- main
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -232,11 +220,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; SPGEMM_DIST_BACKEND=gloo lets several ranks share one GPU
+    # to exercise the N>1 code path on a single-GPU box (timings then meaningless)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SPGEMM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     ctx = sg.get_context(local)
     peak, peak_kind = load_peaks()
 
@@ -251,33 +246,17 @@ def main():
     else:
         if args.config != 2:
             raise SystemExit("multi-GPU bench runs the weak-scaled 27-point stencil (config 2)")
-        if rank == 0:
-            g = stencil_weak(world)
-            shape = torch.tensor([g.rows, g.nnz()], dtype=torch.int64, device="cuda")
-        else:
-            shape = torch.zeros(2, dtype=torch.int64, device="cuda")
-        dist.broadcast(shape, 0)
-        rows, nnz = int(shape[0]), int(shape[1])
-        if rank == 0:
-            gd = g.to_device(local)
-            grpt, gcol, gval = gd.rpt, gd.col, gd.val
-        else:
-            grpt = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
-            gcol = torch.empty(nnz, dtype=torch.int32, device="cuda")
-            gval = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        from paper_2206_07244_b200.distributed import broadcast_csr, nprod_split, slice_rows
+        g = stencil_weak(world) if rank == 0 else None
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
-        for t in (grpt, gcol, gval):  # B replicated over NVLink (ncclBroadcast)
-            dist.broadcast(t, 0)
+        B = broadcast_csr(g.to_device(local) if rank == 0 else None, 0, torch.device("cuda", local))
         torch.cuda.synchronize()
         bcast_s = time.perf_counter() - t0
-        B = CsrMatrix(rows, rows, grpt, gcol, gval)
-        nprod, _ = sg.compute_nprod(B, B, device=local)
+        nprod, _ = sg.compute_nprod(B, B, device=local)   # K1 on every rank: identical split, no collective
         bounds = nprod_split(nprod, world)
-        r0, r1 = bounds[rank], bounds[rank + 1]
-        p0, p1 = int(grpt[r0]), int(grpt[r1])
-        A_loc = CsrMatrix(r1 - r0, rows, grpt[r0:r1 + 1] - p0, gcol[p0:p1], gval[p0:p1])
+        A_loc = slice_rows(B, bounds[rank], bounds[rank + 1])
         pairs = [(A_loc, B)]
         host_ops = None
         workload = f"C=A*A 3D 27-pt stencil 128x128x{128 * world} (weak: 128^3 rows/GPU), nprod-balanced row blocks"

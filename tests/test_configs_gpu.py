@@ -70,3 +70,16 @@ def test_device_resident_inputs(sg, oracle):
     dm.free()
     assert_matches_oracle(c, oracle.spgemm(a, a))
     assert rep.stats.total_nprod == oracle.compute_nprod(a, a)[1]
+
+
+def test_virtual_row_slices_stitch_bitwise(sg, oracle):
+    """SURVEY §8(e) on one GPU: G nprod-balanced row blocks multiplied separately and
+    stitched equal the single-shot product bitwise."""
+    from paper_2206_07244_b200.distributed import nprod_split, slice_rows, stitch
+    a = S.random_values(S.stencil3d_27pt(24), 3)
+    single = sg.multiply(a, a).c
+    nprod, _ = sg.compute_nprod(a, a)
+    for parts in (2, 3, 8):
+        b = nprod_split(nprod, parts)
+        slices = [sg.multiply(slice_rows(a, b[g], b[g + 1]), a).c for g in range(parts)]
+        assert stitch(slices, a.cols) == single

@@ -1,0 +1,102 @@
+"""CPU, world_size 2 (gloo on 127.0.0.1): the multi-GPU logic of SURVEY.md §8(e) --
+B broadcast, deterministic nprod-balanced row split, per-rank block products,
+row-pointer stitching -- checked bitwise against the single-shot oracle product.
+The per-rank multiply is the oracle here (no GPU in the CPU suite); on the B200 box
+the same code runs the sm_100a library over NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from helpers import random_csr
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_2206_07244_b200.distributed import multiply_distributed
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if case == "square":
+            a = random_csr(700, 700, 0.02, 5) if rank == 0 else None
+            b, same = a, True
+        else:
+            a = random_csr(333, 250, 0.04, 6) if rank == 0 else None
+            b = random_csr(250, 410, 0.03, 7) if rank == 0 else None
+            same = False
+        res = multiply_distributed(a, b, same=same, gather_to=0,
+                                   local_multiply=O.spgemm, local_nprod=lambda x, y: O.compute_nprod(x, y)[0])
+        out = dict(rank=rank, bounds=res.row_bounds, offsets=res.nnz_offsets, nnz=int(res.c_local.nnz()),
+                   total_nprod=res.total_nprod)
+        if rank == 0:
+            exp = O.spgemm(a, b)
+            c = res.c
+            out["same_pattern"] = bool(np.array_equal(c.rpt, exp.rpt) and np.array_equal(c.col, exp.col))
+            out["bitwise"] = bool(np.array_equal(c.val.view(np.int64), exp.val.view(np.int64)))
+            nprod, total = O.compute_nprod(a, b)
+            out["exp_total_nprod"] = total
+            b0, b1, b2 = res.row_bounds
+            out["halves"] = (int(nprod[b0:b1].sum()), int(nprod[b1:b2].sum()))
+        q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["square", "rect"])
+def test_two_rank_gloo_matches_single_shot(case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    outs.sort(key=lambda d: d["rank"])
+    r0, r1 = outs
+    assert r0["bounds"] == r1["bounds"]                  # same split derived independently
+    assert r0["offsets"] == r1["offsets"] == [0, r0["nnz"]]
+    assert r0["same_pattern"] and r0["bitwise"]
+    assert r0["total_nprod"] == r0["exp_total_nprod"]
+    lo, hi = r0["halves"]
+    assert abs(lo - hi) <= max(lo, hi) * 0.05 + 400     # balanced by nprod
+
+
+def test_nprod_split_properties():
+    from paper_2206_07244_b200.distributed import nprod_split
+    rng = np.random.default_rng(0)
+    nprod = rng.integers(0, 1000, 10_000)
+    for parts in (1, 2, 3, 8):
+        b = nprod_split(nprod, parts)
+        assert b[0] == 0 and b[-1] == nprod.size and len(b) == parts + 1
+        assert all(x <= y for x, y in zip(b, b[1:]))
+        sums = [nprod[b[g]:b[g + 1]].sum() for g in range(parts)]
+        assert max(sums) - min(sums) <= 2 * nprod.max() + 1
+    assert nprod_split(np.zeros(5, np.int64), 2) == [0, 2, 5]
+    assert nprod_split(np.zeros(0, np.int64), 3) == [0, 0, 0, 0]
+
+
+def test_stitch_offsets():
+    from paper_2206_07244_b200.api import CsrMatrix
+    from paper_2206_07244_b200.distributed import slice_rows, stitch
+    a = random_csr(50, 40, 0.1, 3)
+    parts = [slice_rows(a, 0, 17), slice_rows(a, 17, 17), slice_rows(a, 17, 50)]
+    s = stitch(parts, a.cols)
+    assert isinstance(s, CsrMatrix) and s == a
