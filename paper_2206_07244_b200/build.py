@@ -15,7 +15,10 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libspgemm_b200.so")
 SOURCES = [os.path.join(CSRC, "capi.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "kernels.cuh"), os.path.join(ROOT, "include", "spgemm_capi.h")]
+CXX_SOURCES = [os.path.join(CSRC, "cxx_api.cpp")]  # the reference's C++ API over the C ABI
+HEADERS = [os.path.join(ROOT, "include", "spgemm_capi.h")] + [
+    os.path.join(ROOT, "include", "spgemm", h) for h in sorted(os.listdir(os.path.join(ROOT, "include", "spgemm")))]
+DEPS = SOURCES + CXX_SOURCES + HEADERS + [os.path.join(CSRC, "kernels.cuh")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -44,7 +47,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES]
+    objs = []
+    for src in CXX_SOURCES:
+        obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
+        cc = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+              "-c", src, "-o", obj]
+        r = subprocess.run(cc, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"g++ failed on {src}")
+        objs.append(obj)
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES, *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(LIBDIR, "ptxas.log")
     with open(log, "w") as f:
