@@ -307,8 +307,8 @@ struct spgemm_pipeline {
   int64_t* d_rpt = nullptr;
   unsigned char* d_arena = nullptr;
   size_t arena_bytes = 0;
-  int32_t* d_bins = nullptr;
-  int32_t* d_spill = nullptr;
+  int64_t* d_bins = nullptr;
+  int64_t* d_spill = nullptr;
   int32_t* d_blk = nullptr;
   int* d_flags = nullptr;
   long long* d_sums = nullptr;
@@ -412,10 +412,10 @@ void spgemm_pipeline::setup() {
   off = align_up(off + static_cast<size_t>(ntiles) * 4, 256);
   const size_t o_sums = off;
   off = align_up(off + static_cast<size_t>(ntiles) * 16, 256);
-  const size_t o_bins = off;
-  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 4, 256);
+  const size_t o_bins = off;  // row ids as int64, the reference's BinningResult layout
+  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
   const size_t o_spill = off;
-  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 4, 256);
+  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
   arena_bytes = off;
   d_arena = static_cast<unsigned char*>(dev_alloc(arena_bytes, s));
   metadata_calls += 1;
@@ -425,8 +425,8 @@ void spgemm_pipeline::setup() {
   d_blk = reinterpret_cast<int32_t*>(d_arena + o_blk);
   d_flags = reinterpret_cast<int*>(d_arena + o_flags);
   d_sums = reinterpret_cast<long long*>(d_arena + o_sums);
-  d_bins = reinterpret_cast<int32_t*>(d_arena + o_bins);
-  d_spill = reinterpret_cast<int32_t*>(d_arena + o_spill);
+  d_bins = reinterpret_cast<int64_t*>(d_arena + o_bins);
+  d_spill = reinterpret_cast<int64_t*>(d_arena + o_spill);
   ck(cudaMemsetAsync(d_info_sym, 0, 2 * sizeof(DevInfo), s), "memset info");
   if (M > 0) {
     SPG_LAUNCH(ctx, "k_setup_nprod", s,
@@ -589,10 +589,10 @@ void spgemm_pipeline::numeric_binning() {
     fail(SPGEMM_OVERFLOW, "spgemm: nonzero count overflowed 64 bits");
   total_nnz = static_cast<int64_t>(h_num.total);
   if (opts.overlap) {
-    ck(cudaStreamWaitEvent(ctx->side_s, ctx->ev_info, 0), "side wait");
-    allocate_output(ctx->side_s);
-    ck(cudaEventRecord(ctx->ev_side, ctx->side_s), "ev_side");
-    alloc_pending = true;
+    // C.col/C.val are allocated now, stream-ordered behind the scatter that is
+    // still running (the allocation lane of pipeline.cpp:254-257). Same stream
+    // as the previous product's free, so the pool reuses that memory directly.
+    allocate_output(s);
   }
   bin_info.max_metric = h_num.max_metric;
   bin_info.total_metric = total_nnz;
@@ -617,12 +617,7 @@ int64_t spgemm_pipeline::finalize_rpt() {
   fetch_info(d_info_num, &tmp);
   if (tmp.scan_total != total_nnz)
     fail(SPGEMM_LOGIC_ERROR, "spgemm: exclusive sum disagrees with binning total");
-  if (alloc_pending) {
-    ck(cudaStreamWaitEvent(s, ctx->ev_side, 0), "join alloc lane");
-    alloc_pending = false;
-  } else {
-    allocate_output(s);
-  }
+  if (!d_ccol) allocate_output(s);  // overlap=false: allocate only now
   mark(9);
   stage = kRptDone;
   return total_nnz;
@@ -1052,12 +1047,10 @@ spgemm_status spgemm_pipeline_binning(spgemm_pipeline* p, spgemm_binning_info* i
                  k_iota<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(p->M, 256), 4096)), 256, 0,
                p->ctx->main_s>>>(p->d_bins, p->M));
     }
-    std::vector<int32_t> tmp(static_cast<size_t>(p->M));
-    ck(cudaMemcpyAsync(tmp.data(), p->d_bins, static_cast<size_t>(p->M) * 4,
-                       cudaMemcpyDeviceToHost, p->ctx->main_s),
+    ck(cudaMemcpyAsync(bins_host, p->d_bins, static_cast<size_t>(p->M) * 8, cudaMemcpyDeviceToHost,
+                       p->ctx->main_s),
        "D2H bins");
     ck(cudaStreamSynchronize(p->ctx->main_s), "cudaStreamSynchronize");
-    for (int64_t i = 0; i < p->M; ++i) bins_host[i] = tmp[static_cast<size_t>(i)];
   });
 }
 
@@ -1204,7 +1197,7 @@ spgemm_status spgemm_run_binning(spgemm_ctx* ctx, const int64_t* metric, int64_t
     const BinUpper up = to_upper(*cfg);
     const int64_t nrb = ceil_div(m, kRowsPerBlock);
     auto* d_metric = static_cast<int64_t*>(dev_alloc(static_cast<size_t>(m) * 8, s));
-    auto* d_bins = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(m) * 4, s));
+    auto* d_bins = static_cast<int64_t*>(dev_alloc(static_cast<size_t>(m) * 8, s));
     auto* d_blk = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(nrb) * kNumBins * 4, s));
     auto* d_info = static_cast<DevInfo*>(dev_alloc(sizeof(DevInfo), s));
     ck(cudaMemcpyAsync(d_metric, metric, static_cast<size_t>(m) * 8, cudaMemcpyHostToDevice, s), "H2D");
@@ -1223,11 +1216,8 @@ spgemm_status spgemm_run_binning(spgemm_ctx* ctx, const int64_t* metric, int64_t
       SPG_LAUNCH(ctx, "k_iota", s,
                  k_iota<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(m, 256), 4096)), 256, 0, s>>>(d_bins, m));
     }
-    std::vector<int32_t> tmp(static_cast<size_t>(m));
-    ck(cudaMemcpyAsync(tmp.data(), d_bins, static_cast<size_t>(m) * 4, cudaMemcpyDeviceToHost, s),
-       "D2H bins");
+    ck(cudaMemcpyAsync(bins_host, d_bins, static_cast<size_t>(m) * 8, cudaMemcpyDeviceToHost, s), "D2H bins");
     ck(cudaStreamSynchronize(s), "sync");
-    for (int64_t i = 0; i < m; ++i) bins_host[i] = tmp[static_cast<size_t>(i)];
     for (int j = 0; j < kNumBins; ++j) {
       bi.bin_size[j] = hi.bin_size[j];
       bi.bin_offset[j] = hi.bin_offset[j];

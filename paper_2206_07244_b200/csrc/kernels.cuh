@@ -70,12 +70,12 @@ constexpr int kErrTableFull = 2;
 
 // Rows of one bin: either the identity (fast path) or a segment of bins[].
 struct RowList {
-  const int32_t* __restrict__ bins;
+  const int64_t* __restrict__ bins;
   long long offset;
   long long count;
   int identity;
   __device__ __forceinline__ int64_t row(int64_t idx) const {
-    return identity ? idx : static_cast<int64_t>(bins[offset + idx]);
+    return identity ? idx : bins[offset + idx];
   }
 };
 
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(1024)
 // (binning.cpp:205-241), whatever the chunk size. Skipped on the fast path.
 __global__ void __launch_bounds__(kBinThreads)
     k_bin_scatter(const int64_t* __restrict__ metric, int64_t M, BinUpper up,
-                  const int32_t* __restrict__ blk_offsets, int32_t* __restrict__ bins,
+                  const int32_t* __restrict__ blk_offsets, int64_t* __restrict__ bins,
                   const DevInfo* info) {
   if (info->fast_path) return;
   constexpr int NW = kBinThreads / 32;
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kBinThreads)
     if (valid) {
       int pos = s_run[bin] + rank;
       for (int w = 0; w < warp; ++w) pos += s_wcnt[w][bin];
-      bins[pos] = static_cast<int32_t>(row);
+      bins[pos] = row;
     }
     __syncthreads();
     if (threadIdx.x < kNumBins) {
@@ -483,10 +483,10 @@ __global__ void __launch_bounds__(kBinThreads)
   }
 }
 
-__global__ void k_iota(int32_t* out, int64_t n) {
+__global__ void k_iota(int64_t* out, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[i] = static_cast<int32_t>(i);
+    out[i] = i;
 }
 
 // K5: single-pass in-place exclusive scan (decoupled look-back) of n int64.
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(G* NGRP)
 template <int T, int THREADS, bool SPILL>
 __global__ void __launch_bounds__(THREADS)
     k_sym_block(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale,
-                int32_t* __restrict__ spill_ids, DevInfo* info, int thresh) {
+                int64_t* __restrict__ spill_ids, DevInfo* info, int thresh) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw);
   __shared__ int s_cnt, s_abort;
@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(THREADS)
       if (threadIdx.x == 0) {
         if (s_abort) {
           const unsigned long long i = atomicAdd(&info->spill_count, 1ull);
-          spill_ids[i] = static_cast<int32_t>(row);
+          spill_ids[i] = row;
         } else {
           rpt[row] = s_cnt;
         }
@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(THREADS)
 // global-memory table. Instead of one heap table per row, each resident block
 // reuses one region of a pool; the row's table is bit_ceil(2*min(nprod, cols)).
 __global__ void __launch_bounds__(1024)
-    k_sym_spill(DevCsr A, DevCsr B, int64_t* __restrict__ rpt, const int32_t* __restrict__ spill_ids,
+    k_sym_spill(DevCsr A, DevCsr B, int64_t* __restrict__ rpt, const int64_t* __restrict__ spill_ids,
                 const DevInfo* info, int32_t* __restrict__ pool, int64_t slots_per_block,
                 uint32_t scale) {
   __shared__ long long s_red[32];

@@ -18,5 +18,6 @@ for cfg in cfgs:
         dm, out = sg.multiply_device(a, b)
         torch.cuda.synchronize(); ts.append(time.perf_counter() - t0); dm.free()
     t = min(ts)
+    print(f"  runs ms: {[round(x*1e3, 3) for x in ts]}")
     print(f"cfg{cfg}: wall {t*1e3:.3f} ms  GFLOPS {2*out.stats.total_nprod/t/1e9:.1f}  steps(ms) " +
           " ".join(f"{k}={getattr(out.timings,k)*1e3:.3f}" for k in ("setup","sym_binning","symbolic","num_binning","rpt_alloc","numeric")), flush=True)
