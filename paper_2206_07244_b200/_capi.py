@@ -8,7 +8,12 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from . import build as _build
+import importlib.util as _ilu
+
+# build.py is loaded by path so that it never depends on the library itself
+_spec = _ilu.spec_from_file_location("_spgemm_build", os.path.join(os.path.dirname(__file__), "build.py"))
+_build = _ilu.module_from_spec(_spec)
+_spec.loader.exec_module(_build)
 
 NUM_BINS = 8
 NO_UPPER_BOUND = (1 << 63) - 1
@@ -70,7 +75,7 @@ class Plan(C.Structure):
 
 LIB_PATH = _build.LIB
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2206_07244_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2206_07244_b200/build.py` "
                       "(the CUDA library is the only implementation; there is no CPU fallback)")
 
 lib = C.CDLL(LIB_PATH)
@@ -94,6 +99,7 @@ _decl("spgemm_ctx_synchronize", _st, [_P])
 _decl("spgemm_ctx_stream", _P, [_P])
 _decl("spgemm_ctx_set_profiling", None, [_P, C.c_int32])
 _decl("spgemm_ctx_profile_summary", C.c_int32, [_P, C.POINTER(KernelTime), C.c_int32])
+_decl("spgemm_ctx_pool_stats", _st, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)])
 _decl("spgemm_options_default", None, [C.POINTER(Options)])
 _decl("spgemm_preset", _st, [C.c_int32, C.c_char_p, C.POINTER(BinConfig)])
 _decl("spgemm_classify", C.c_int32, [C.c_int64, C.POINTER(BinConfig)])
@@ -124,7 +130,7 @@ _decl("spgemm_run_binning", _st, [_P, _P, C.c_int64, C.POINTER(BinConfig), C.c_i
 EXPORTED = [
     "spgemm_ctx_create", "spgemm_ctx_destroy", "spgemm_last_error", "spgemm_ctx_device", "spgemm_ctx_num_sms",
     "spgemm_ctx_kernel_launches", "spgemm_ctx_synchronize", "spgemm_ctx_stream", "spgemm_ctx_set_profiling",
-    "spgemm_ctx_profile_summary", "spgemm_options_default",
+    "spgemm_ctx_profile_summary", "spgemm_ctx_pool_stats", "spgemm_options_default",
     "spgemm_preset", "spgemm_classify", "spgemm_make_plan", "spgemm_pipeline_create", "spgemm_pipeline_destroy",
     "spgemm_pipeline_setup", "spgemm_pipeline_symbolic_binning", "spgemm_pipeline_run_symbolic",
     "spgemm_pipeline_numeric_binning", "spgemm_pipeline_finalize_rpt", "spgemm_pipeline_run_numeric",

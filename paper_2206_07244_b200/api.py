@@ -118,6 +118,12 @@ class Context:
         """Bracket every kernel launch with CUDA events on its own stream."""
         _c.lib.spgemm_ctx_set_profiling(self.handle, int(bool(on)))
 
+    def pool_stats(self):
+        """(reserved, used) bytes of the device's stream-ordered memory pool."""
+        r, u = C.c_uint64(), C.c_uint64()
+        _check(_c.lib.spgemm_ctx_pool_stats(self.handle, C.byref(r), C.byref(u)))
+        return r.value, u.value
+
     def profile_summary(self) -> dict:
         """{kernel name: (launches, total ms)} since the last call (synchronises)."""
         buf = (_c.KernelTime * 64)()

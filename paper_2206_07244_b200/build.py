@@ -1,6 +1,6 @@
 """In-tree build of the sm_100a library (no JIT cache: the .so travels with the repo).
 
-``python -m paper_2206_07244_b200.build`` compiles ``csrc/capi.cu`` (which includes
+``python paper_2206_07244_b200/build.py`` compiles ``csrc/capi.cu`` (which includes
 every kernel) into ``paper_2206_07244_b200/lib/libspgemm_b200.so``.
 """
 from __future__ import annotations

@@ -514,6 +514,14 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     dev_free(pool, s);
     return;
   }
+  if (u <= 32) {  // thread per row, private 64-slot table (load <= 1/2)
+    const size_t smem = 256 * 64 * 4;
+    auto kern = &k_sym_thread<64>;
+    prepare_kernel(ctx, kern, smem);
+    const int grid = persistent_grid(ctx, kern, 256, smem, ceil_div(rl.count, 256));
+    SPG_LAUNCH(ctx, "k_sym_thread<64>", s, kern<<<grid, 256, smem, s>>>(rl, A, B, d_rpt, scale));
+    return;
+  }
   // group kernels: (G, T, groups per block, bitmap words per group)
   if (u < 64) {
     if (g8) group(SYMG(8, 64, 32, 256), 8, 64, 32, 256);
@@ -647,6 +655,13 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     SPG_LAUNCH(ctx, "k_num_global", s,
                k_num_global<<<gblocks, kGlobalThreads, 0, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, gkeys,
                                                     gvals, gbits, gslots, gwords, d_info_num));
+  } else if (u <= 16) {  // thread per row: 32-slot private table, 16-key register sort
+    const size_t smem = 128 * 32 * 12;
+    auto kern = &k_num_thread<32, 16>;
+    prepare_kernel(ctx, kern, smem);
+    const int grid = persistent_grid(ctx, kern, 128, smem, ceil_div(rl.count, 128));
+    SPG_LAUNCH(ctx, "k_num_thread<32,16>", s,
+               kern<<<grid, 128, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
   } else if (u <= 32) {
     if (g8) group(NUMG(8, 64, 4, 32), 8, 64, 4, 32);
     else group(NUMG(32, 64, 1, 8), 32, 64, 1, 8);
@@ -859,6 +874,15 @@ int32_t spgemm_ctx_num_sms(const spgemm_ctx* c) { return c->num_sms; }
 int64_t spgemm_ctx_kernel_launches(const spgemm_ctx* c) { return c->launches.load(); }
 
 void spgemm_ctx_set_profiling(spgemm_ctx* c, int32_t on) { c->prof = on != 0; }
+
+spgemm_status spgemm_ctx_pool_stats(spgemm_ctx* c, uint64_t* reserved, uint64_t* used) {
+  return guard([&] {
+    cudaMemPool_t pool;
+    ck(cudaDeviceGetMemPool(&pool, c->device), "cudaDeviceGetMemPool");
+    ck(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, reserved), "pool attr");
+    ck(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, used), "pool attr");
+  });
+}
 
 int32_t spgemm_ctx_profile_summary(spgemm_ctx* c, spgemm_kernel_time* out, int32_t max) {
   int32_t n = 0;

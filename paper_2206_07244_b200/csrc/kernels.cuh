@@ -895,6 +895,137 @@ __global__ void __launch_bounds__(G* NGRP)
   }
 }
 
+// Thread-per-row symbolic kernel for the smallest bin (nprod <= TS/2): each
+// thread owns one row and a private TS-slot table in shared memory laid out
+// interleaved (slot s of lane l at [s*32 + l]: every lane always hits its own
+// bank, whatever slot it probes). No atomics, barriers or shuffles.
+template <int TS>
+__global__ void __launch_bounds__(256)
+    k_sym_thread(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + warp * TS * 32 + lane;
+  const Hash hs = make_hash(scale, log2_const<TS>());
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rl.count; idx += stride) {
+    const int64_t row = rl.row(idx);
+    if (rpt[row] == 0) continue;
+#pragma unroll
+    for (int s = 0; s < TS; ++s) tab[s * 32] = -1;
+    int cnt = 0;
+    const int64_t a1 = A.rpt[row + 1];
+    for (int64_t p = A.rpt[row]; p < a1; ++p) {
+      const int32_t k = A.col[p];
+      const int64_t b1 = B.rpt[k + 1];
+      for (int64_t q = B.rpt[k]; q < b1; ++q) {
+        const int32_t key = B.col[q];
+        uint32_t h = hs.home(key);
+        while (true) {
+          const int32_t c = tab[h * 32];
+          if (c == key) break;
+          if (c == -1) {
+            tab[h * 32] = key;
+            ++cnt;
+            break;
+          }
+          h = (h + 1) & (TS - 1);
+        }
+      }
+    }
+    rpt[row] = cnt;
+  }
+}
+
+// Thread-per-row numeric kernel for rows with nnz <= NMAX (TS = 2*NMAX slots):
+// the thread walks its row in the reference's order (so the fold is trivially
+// the reference's), compacts its private table in place, sorts the NMAX packed
+// (col, slot) keys with a register bitonic network, and writes C(i,:).
+template <int TS, int NMAX>
+__global__ void __launch_bounds__(128)
+    k_num_thread(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale, DevInfo* info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* vals = reinterpret_cast<double*>(smem_raw) + warp * TS * 32 + lane;
+  int32_t* keys = reinterpret_cast<int32_t*>(smem_raw + static_cast<size_t>(blockDim.x) * TS * 8) +
+                  warp * TS * 32 + lane;
+  const Hash hs = make_hash(scale, log2_const<TS>());
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rl.count; idx += stride) {
+    const int64_t row = rl.row(idx);
+    const int64_t base = rpt[row];
+    const int n = static_cast<int>(rpt[row + 1] - base);
+    if (n == 0) continue;
+#pragma unroll
+    for (int s = 0; s < TS; ++s) {
+      keys[s * 32] = -1;
+      vals[s * 32] = 0.0;
+    }
+    const int64_t a1 = A.rpt[row + 1];
+    for (int64_t p = A.rpt[row]; p < a1; ++p) {
+      const int32_t k = A.col[p];
+      const double av = A.val[p];
+      const int64_t b1 = B.rpt[k + 1];
+      for (int64_t q = B.rpt[k]; q < b1; ++q) {
+        const int32_t key = B.col[q];
+        const double x = __dmul_rn(av, B.val[q]);
+        uint32_t h = hs.home(key);
+        while (true) {
+          const int32_t c = keys[h * 32];
+          if (c == key) break;
+          if (c == -1) {
+            keys[h * 32] = key;
+            break;
+          }
+          h = (h + 1) & (TS - 1);
+        }
+        vals[h * 32] = __dadd_rn(vals[h * 32], x);
+      }
+    }
+    // compact in place: entry m <- slot s (m <= s), keys and values together
+    int m = 0;
+#pragma unroll
+    for (int s = 0; s < TS; ++s) {
+      const int32_t c = keys[s * 32];
+      if (c != -1) {
+        keys[m * 32] = c;
+        vals[m * 32] = vals[s * 32];
+        ++m;
+      }
+    }
+    if (m != n) atomicOr(&info->error, kErrNumericCount);
+    unsigned long long v[NMAX];
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i)
+      v[i] = i < m ? (static_cast<unsigned long long>(static_cast<uint32_t>(keys[i * 32])) << 32) | static_cast<uint32_t>(i)
+                   : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= NMAX; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+        for (int i = 0; i < NMAX; ++i) {
+          const int pi = i ^ j;
+          if (pi > i) {
+            const bool up = (i & k) == 0;
+            const unsigned long long a = v[i], b = v[pi];
+            const bool sw = up ? (a > b) : (a < b);
+            v[i] = sw ? b : a;
+            v[pi] = sw ? a : b;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      if (i < m) {
+        ccol[base + i] = static_cast<int32_t>(v[i] >> 32);
+        cval[base + i] = vals[static_cast<uint32_t>(v[i]) * 32];
+      }
+    }
+  }
+}
+
 // Block kernel: one row per block iteration, warps take A entries, lanes
 // stride B rows. SPILL (the last bin): the fixed table aborts a row once its
 // distinct count exceeds the reference's 0.8*24575 = 19660 threshold
