@@ -56,55 +56,56 @@ def load_peaks():
 
 # -------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled in-process through NVML every 200 ms
+    during the timed region (nvidia-smi polling contends with the CUDA driver
+    and perturbs a ms-scale step loop; tools/sampler_probe.py measures it)."""
 
-    def __init__(self, index=0):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    REASONS = {  # NVML clocks-event-reason bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index=0, period=0.2):
+        self.index, self.period = index, period
+        self.samples = []
+        self._stop = threading.Event()
+        self.ok = False
+
+    def _sample(self):
+        import pynvml
+        self.samples.append((time.time(), pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM),
+                             pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-            time.sleep(0.3)
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            return
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
+        def run():
+            while not self._stop.is_set():
+                self._sample()
+                self._stop.wait(self.period)
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
 
     def stop(self):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-        self.t_stop = time.time()
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+            self._sample()  # always at least one sample at the end of the region
 
     def summary(self, t0, t1):
-        rows = []
-        for ts, line in self.lines:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 6:
-                continue
-            rows.append((ts, parts))
-        inwin = [r for r in rows if t0 - 0.06 <= r[0] <= t1 + 0.06] or rows
-        if not inwin:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(p[0]) for _, p in inwin if p[0].replace(".", "").isdigit()]
-        smax = [float(p[1]) for _, p in inwin if p[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, p in inwin for i in range(4) if p[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(inwin)}
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        inwin = [x for x in self.samples if t0 - 0.25 <= x[0] <= t1 + 0.25] or self.samples
+        reasons = sorted({n for _, _, bits in inwin for n, b in self.REASONS.items() if bits & b})
+        return {"sm_mhz": statistics.median(c for _, c, _ in inwin), "sm_max_mhz": self.max_sm,
+                "reasons": reasons, "samples": len(inwin), "source": "nvml"}
 
 
 # -------------------------------------------------------- CPU baseline
@@ -297,33 +298,51 @@ def main():
     torch.cuda.synchronize()
 
     # ------------------------------------------------------------- timed
+    # Pass 1 (value): K steps bracketed by barrier + synchronize, CUDA events on
+    # the library's stream. Pass 2 (roofline): the same K steps again with every
+    # kernel bracketed by events on its own stream (per-kernel device time), so
+    # the per-launch events cannot perturb pass 1.
+    import gc
     stream = torch.cuda.ExternalStream(ctx.stream)
     clocks = ClockSampler(local)
+
+    def timed_pass(profile):
+        if profile:
+            ctx.profile_summary()  # clear
+            ctx.set_profiling(True)
+        launches0 = ctx.kernel_launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        gc.disable()
+        tw0 = time.time()
+        ev0.record(stream)
+        tot = 0
+        dbg = os.environ.get("SPGEMM_BENCH_DEBUG")
+        for _ in range(args.steps):
+            ts = time.perf_counter()
+            tot += one_step()
+            if dbg:
+                print(f"step {1e3 * (time.perf_counter() - ts):.3f} ms", file=sys.stderr)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        tw1 = time.time()
+        gc.enable()
+        if dist:
+            dist.barrier()
+        kern = None
+        if profile:
+            ctx.set_profiling(False)
+            kern = ctx.profile_summary()
+        return ev0.elapsed_time(ev1), tot, ctx.kernel_launches - launches0, kern, tw0, tw1
+
     if rank == 0:
         clocks.start()
-    ctx.profile_summary()  # clear
-    ctx.set_profiling(True)
-    launches0 = ctx.kernel_launches
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    tw0 = time.time()
-    ev0.record(stream)
-    total_nprod = 0
-    for _ in range(args.steps):
-        total_nprod += one_step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    tw1 = time.time()
-    if dist:
-        dist.barrier()
-    ctx.set_profiling(False)
-    kernels = ctx.profile_summary()
-    launches = ctx.kernel_launches - launches0
+    t_ms, total_nprod, launches, _, tw0, tw1 = timed_pass(False)
     if rank == 0:
         clocks.stop()
-    t_ms = ev0.elapsed_time(ev1)
+    t_prof_ms, _, _, kernels, _, _ = timed_pass(True)
     t_max = t_ms
     nprod_all = total_nprod
     if dist:
@@ -393,7 +412,7 @@ def main():
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": kernel_bytes, "avg_launch_ms": avg_s * 1e3,
-                "share_of_step": ms_total / t_ms}
+                "share_of_step": ms_total / t_prof_ms, "profiled_pass_ms_per_step": t_prof_ms / args.steps}
         step_roof = {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,
                      "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
 

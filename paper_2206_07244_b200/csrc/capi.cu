@@ -303,6 +303,7 @@ struct spgemm_pipeline {
   uint32_t scale = 107;
   double avg_b_len = 0;
   bool idx32 = true;
+  bool sym_bins_on_device = false;
 
   int64_t* d_rpt = nullptr;
   unsigned char* d_arena = nullptr;
@@ -348,7 +349,7 @@ struct spgemm_pipeline {
   void symbolic_binning();
   void run_symbolic();
   void numeric_binning();
-  int64_t finalize_rpt();
+  int64_t finalize_rpt(bool host_total = true);
   void run_numeric();
   void finish(spgemm_report* r);
   void allocate_output(cudaStream_t s);
@@ -460,13 +461,9 @@ void spgemm_pipeline::symbolic_binning() {
     SPG_LAUNCH(ctx, "k_bin_scatter", s,
                k_bin_scatter<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(d_rpt, M, sym_up, d_blk,
                                                                       d_bins, d_info_sym));
-    DevInfo tmp;
-    fetch_info(d_info_sym, &tmp);
-    h_sym.spill_count = tmp.spill_count;
-    for (int j = 0; j < kNumBins; ++j) {
-      bin_info.bin_size[j] = tmp.bin_size[j];
-      bin_info.bin_offset[j] = tmp.bin_offset[j];
-    }
+    // No host round trip: the symbolic kernels read their bin's size and
+    // offset from d_info_sym; binning() fetches them only if asked.
+    sym_bins_on_device = true;
   }
   mark(3);
   stage = kSymBinned;
@@ -548,12 +545,19 @@ void spgemm_pipeline::run_symbolic() {
   expect(kSymBinned, "run_symbolic");
   mark(4);
   ck(cudaEventRecord(ctx->ev_fork, ctx->main_s), "ev_fork");
+  // bins above the one holding the max nprod are empty (max known since setup)
+  int top = kNumBins - 1;
+  while (top > 0 && h_sym.max_metric <= sym_plan.config.upper[top - 1]) --top;
   for (int r = 0; r < kNumBins; ++r) {
     const int bin = sym_plan.launch_order[r];
-    if (bin_info.bin_size[bin] == 0) continue;
+    if (sym_bins_on_device ? bin > top : bin_info.bin_size[bin] == 0) continue;
     cudaStream_t s = ctx->bin_s[bin];
     ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
-    RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path};
+    // device-resolved row list: `count` only sizes the persistent grid
+    RowList rl = sym_bins_on_device
+                     ? RowList{d_bins, 0, M, 0, d_info_sym, bin}
+                     : RowList{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path,
+                               nullptr, bin};
     launch_sym_bin(bin, rl, s);
     ck(cudaEventRecord(ctx->ev_join[bin], s), "ev_join");
     ck(cudaStreamWaitEvent(ctx->main_s, ctx->ev_join[bin], 0), "wait join");
@@ -613,7 +617,7 @@ void spgemm_pipeline::numeric_binning() {
   stage = kNumBinned;
 }
 
-int64_t spgemm_pipeline::finalize_rpt() {
+int64_t spgemm_pipeline::finalize_rpt(bool host_total) {
   expect(kNumBinned, "finalize_rpt");
   mark(8);
   cudaStream_t s = ctx->main_s;
@@ -621,10 +625,14 @@ int64_t spgemm_pipeline::finalize_rpt() {
   SPG_LAUNCH(ctx, "k_scan", s,
              k_scan<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(d_rpt, M + 1, d_flags, d_sums,
                                                                  d_sums + ntiles, d_info_num));
-  DevInfo tmp;
-  fetch_info(d_info_num, &tmp);
-  if (tmp.scan_total != total_nnz)
-    fail(SPGEMM_LOGIC_ERROR, "spgemm: exclusive sum disagrees with binning total");
+  // The scan total is cross-checked against the pass-1 total on the device
+  // (kErrScanMismatch, raised at finish); the step API reads it back now.
+  if (host_total) {
+    DevInfo tmp;
+    fetch_info(d_info_num, &tmp);
+    if (tmp.scan_total != total_nnz)
+      fail(SPGEMM_LOGIC_ERROR, "spgemm: exclusive sum disagrees with binning total");
+  }
   if (!d_ccol) allocate_output(s);  // overlap=false: allocate only now
   mark(9);
   stage = kRptDone;
@@ -711,7 +719,7 @@ void spgemm_pipeline::run_numeric() {
     if (bin_info.bin_size[bin] == 0) continue;
     cudaStream_t s = ctx->bin_s[bin];
     ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
-    RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path};
+    RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path, nullptr, bin};
     launch_num_bin(bin, rl, s, gkeys, gvals, gbits, gslots, gwords, gblocks);
     ck(cudaEventRecord(ctx->ev_join[bin], s), "ev_join");
     ck(cudaStreamWaitEvent(ctx->main_s, ctx->ev_join[bin], 0), "wait join");
@@ -725,9 +733,12 @@ void spgemm_pipeline::run_numeric() {
 
 void spgemm_pipeline::finish(spgemm_report* r) {
   expect(kNumeric, "finish");
-  DevInfo sym, num;
-  fetch_info(d_info_sym, &sym);
-  fetch_info(d_info_num, &num);
+  ck(cudaMemcpyAsync(ctx->h_info, d_info_sym, 2 * sizeof(DevInfo), cudaMemcpyDeviceToHost, ctx->main_s),
+     "D2H infos");
+  ck(cudaStreamSynchronize(ctx->main_s), "cudaStreamSynchronize");
+  const DevInfo sym = ctx->h_info[0], num = ctx->h_info[1];
+  if (num.error & kErrScanMismatch)
+    fail(SPGEMM_LOGIC_ERROR, "spgemm: exclusive sum disagrees with binning total");
   if (num.error & kErrNumericCount)
     fail(SPGEMM_LOGIC_ERROR, "spgemm: numeric row nnz disagrees with symbolic result");
   spgemm_report rep;
@@ -1040,7 +1051,7 @@ spgemm_status spgemm_pipeline_run(spgemm_pipeline* p, spgemm_report* r) {
     p->symbolic_binning();
     p->run_symbolic();
     p->numeric_binning();
-    p->finalize_rpt();
+    p->finalize_rpt(false);
     p->run_numeric();
     p->finish(r);
   });
@@ -1062,6 +1073,15 @@ spgemm_status spgemm_pipeline_binning(spgemm_pipeline* p, spgemm_binning_info* i
                                       int64_t* bins_host) {
   return guard([&] {
     DeviceGuard g(p->ctx->device);
+    if (p->sym_bins_on_device && p->stage >= spgemm_pipeline::kSymBinned &&
+        p->stage < spgemm_pipeline::kNumBinned && p->d_arena) {
+      DevInfo tmp;
+      p->fetch_info(p->d_info_sym, &tmp);
+      for (int j = 0; j < kNumBins; ++j) {
+        p->bin_info.bin_size[j] = tmp.bin_size[j];
+        p->bin_info.bin_offset[j] = tmp.bin_offset[j];
+      }
+    }
     if (info) *info = p->bin_info;
     if (!bins_host || p->M == 0) return;
     if (p->stage < spgemm_pipeline::kSymBinned || !p->d_arena)

@@ -67,6 +67,7 @@ struct DevInfo {
 
 constexpr int kErrNumericCount = 1;
 constexpr int kErrTableFull = 2;
+constexpr int kErrScanMismatch = 4;
 
 // Rows of one bin: either the identity (fast path) or a segment of bins[].
 struct RowList {
@@ -74,10 +75,26 @@ struct RowList {
   long long offset;
   long long count;
   int identity;
+  // When set, offset/count/identity are read from the phase's device-side
+  // binning result instead (no host round trip between binning and launch).
+  const DevInfo* dev;
+  int bin;
   __device__ __forceinline__ int64_t row(int64_t idx) const {
     return identity ? idx : bins[offset + idx];
   }
+  __device__ __forceinline__ RowList resolved() const;
 };
+
+__device__ __forceinline__ RowList RowList::resolved() const {
+  RowList r = *this;
+  if (dev) {
+    r.identity = dev->fast_path;
+    r.count = dev->bin_size[bin];
+    r.offset = dev->bin_offset[bin];
+  }
+  return r;
+}
+
 
 __device__ __forceinline__ int classify_bin(long long v, const BinUpper& up) {
   int j = 0;
@@ -542,7 +559,10 @@ __global__ void __launch_bounds__(kScanThreads)
       atomicExch(&flags[tile], 2);
     }
     s_excl = excl;
-    if ((static_cast<int64_t>(tile) + 1) * kScanTile >= n) info->scan_total = excl + agg;
+    if ((static_cast<int64_t>(tile) + 1) * kScanTile >= n) {
+      info->scan_total = excl + agg;
+      if (static_cast<unsigned long long>(excl + agg) != info->total) atomicOr(&info->error, kErrScanMismatch);
+    }
   }
   __syncthreads();
   long long run = s_excl + texcl;
@@ -835,7 +855,8 @@ __device__ __forceinline__ int ceil_log2_ll(long long x) {  // x >= 1
 // (2*nprod slots, capped at T > the bin's nprod bound, so it never fills).
 template <int G, int T, int NGRP, typename IT, int WB>
 __global__ void __launch_bounds__(G* NGRP)
-    k_sym_group(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+    k_sym_group(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+  const RowList rl = rl_in.resolved();
   static_assert(WB >= T, "bitmap region doubles as the hash table");
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -901,7 +922,8 @@ __global__ void __launch_bounds__(G* NGRP)
 // bank, whatever slot it probes). No atomics, barriers or shuffles.
 template <int TS>
 __global__ void __launch_bounds__(256)
-    k_sym_thread(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+    k_sym_thread(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+  const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + warp * TS * 32 + lane;
@@ -942,8 +964,9 @@ __global__ void __launch_bounds__(256)
 // (col, slot) keys with a register bitonic network, and writes C(i,:).
 template <int TS, int NMAX>
 __global__ void __launch_bounds__(128)
-    k_num_thread(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+    k_num_thread(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                  int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale, DevInfo* info) {
+  const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* vals = reinterpret_cast<double*>(smem_raw) + warp * TS * 32 + lane;
@@ -1032,8 +1055,9 @@ __global__ void __launch_bounds__(128)
 // (hash_tables.hpp:18-21) and queues it for k_sym_spill.
 template <int T, int THREADS, bool SPILL>
 __global__ void __launch_bounds__(THREADS)
-    k_sym_block(RowList rl, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale,
+    k_sym_block(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale,
                 int64_t* __restrict__ spill_ids, DevInfo* info, int thresh) {
+  const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw);
   __shared__ int s_cnt, s_abort;
@@ -1195,9 +1219,10 @@ __device__ __forceinline__ void group_sort_inplace(K* buf, int n, int lane, unsi
 // row's column span allows (64 bits otherwise).
 template <int G, int T, int E, int NGRP, typename IT>
 __global__ void __launch_bounds__(G* NGRP)
-    k_num_group(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+    k_num_group(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
                 DevInfo* info) {
+  const RowList rl = rl_in.resolved();
   constexpr int NMAX = G * E;
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1315,9 +1340,10 @@ __device__ __forceinline__ void block_bitonic_smem(unsigned long long* a, int np
 // memory, ordered steps with a block barrier per A entry.
 template <int T, int THREADS, int NMAX>
 __global__ void __launch_bounds__(THREADS)
-    k_num_block(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+    k_num_block(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
                 DevInfo* info) {
+  const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* vals = reinterpret_cast<double*>(smem_raw);
   unsigned long long* packed = reinterpret_cast<unsigned long long*>(smem_raw + T * 8);
@@ -1383,11 +1409,12 @@ __global__ void __launch_bounds__(THREADS)
 // scan gives each entry its output position directly (columns are distinct).
 constexpr int kGlobalThreads = 512;
 __global__ void __launch_bounds__(kGlobalThreads)
-    k_num_global(RowList rl, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+    k_num_global(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                  int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
                  int32_t* __restrict__ pool_keys, double* __restrict__ pool_vals,
                  uint32_t* __restrict__ pool_bits, int64_t slots_per_block, int64_t words_per_block,
                  DevInfo* info) {
+  const RowList rl = rl_in.resolved();
   __shared__ long long s_red[32];
   __shared__ int s_min, s_max;
   int32_t* keys = pool_keys + static_cast<int64_t>(blockIdx.x) * slots_per_block;
