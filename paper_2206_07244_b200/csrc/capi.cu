@@ -18,6 +18,8 @@
 #include <chrono>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <tuple>
 #include <mutex>
 #include <new>
 #include <string>
@@ -171,6 +173,7 @@ struct spgemm_ctx {
   std::atomic<int64_t> launches{0};
   std::mutex attr_mu;
   std::unordered_set<const void*> attr_done;
+  std::map<std::tuple<const void*, int, size_t>, int> occupancy;  // per-kernel resident blocks/SM
   // Optional per-kernel timing: events bracket every launch on its own stream.
   bool prof = false;
   struct ProfRec {
@@ -212,8 +215,18 @@ void prepare_kernel(spgemm_ctx* ctx, Kern kern, size_t smem) {
 template <typename Kern>
 int persistent_grid(spgemm_ctx* ctx, Kern kern, int threads, size_t smem, int64_t work) {
   int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
-     "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  {
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), threads, smem);
+    std::lock_guard<std::mutex> lock(ctx->attr_mu);
+    auto it = ctx->occupancy.find(key);
+    if (it != ctx->occupancy.end()) {
+      per_sm = it->second;
+    } else {
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
+         "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      ctx->occupancy[key] = per_sm;
+    }
+  }
   if (per_sm < 1) fail(SPGEMM_CUDA_ERROR, "kernel cannot be resident (shared memory too large)");
   const int64_t cap = static_cast<int64_t>(per_sm) * ctx->num_sms;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(work, cap)));

@@ -665,7 +665,11 @@ __device__ __forceinline__ int walk_row(const DevCsr& A, const DevCsr& B, int64_
 template <int G, int U>
 __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
                                              int lane, unsigned gm, EntryMeta* meta, int32_t* keys,
-                                             double* vals, const Hash& hs, uint32_t dummy) {
+                                             double* vals, const Hash& hs, uint32_t dummy, int32_t* kmin_out,
+                                             int32_t* kmax_out) {
+  // The row's column range, from the first/last column of each (sorted) B row:
+  // two extra loads per A entry instead of a min/max pass over the table.
+  int32_t kmin = 0x7fffffff, kmax = -1;
   for (int64_t c0 = a0; c0 < a1; c0 += G) {
     const int nc = static_cast<int>(min(static_cast<int64_t>(G), a1 - c0));
     int len = 0;
@@ -675,6 +679,10 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
       const int64_t r0 = B.rpt[k];
       len = static_cast<int>(B.rpt[k + 1] - r0);
       meta[lane] = EntryMeta{static_cast<int32_t>(r0), len, av};
+      if (len > 0) {
+        kmin = min(kmin, B.col[r0]);
+        kmax = max(kmax, B.col[r0 + len - 1]);
+      }
     }
     const int maxlen = group_max<G>(len, gm);
     __syncwarp(gm);
@@ -716,6 +724,13 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
     }
     __syncwarp(gm);
   }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(gm, kmin, o, G));
+    kmax = max(kmax, __shfl_xor_sync(gm, kmax, o, G));
+  }
+  *kmin_out = kmin;
+  *kmax_out = kmax;
 }
 
 // Unordered walk of ONE staged chunk (the symbolic phase has no summation
@@ -1250,9 +1265,10 @@ __global__ void __launch_bounds__(G* NGRP)
     fill_empty<G>(keys, tsz, lane);
     fill_zero<G>(vals, tsz, lane);
     __syncwarp(gm);
+    int kmin = 0x7fffffff, kmax = -1;
     if constexpr (sizeof(IT) == 4) {
       walk_row_num<G, 4>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta, keys, vals, hs,
-                         static_cast<uint32_t>(T));
+                         static_cast<uint32_t>(T), &kmin, &kmax);
     } else {
       walk_row<G, 4, true, true, IT>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
                                      [keys, vals, hs](int32_t key, double x) {
@@ -1261,19 +1277,19 @@ __global__ void __launch_bounds__(G* NGRP)
                                        return 0;
                                      });
     }
-    // column range of the row, for the 32-bit sort key
-    int kmin = 0x7fffffff, kmax = -1;
-    for (int s = lane; s < tsz; s += G) {
-      const int32_t key = keys[s];
-      if (key != -1) {
-        kmin = min(kmin, key);
-        kmax = max(kmax, key);
+    if constexpr (sizeof(IT) != 4) {  // 64-bit index path: range from the table
+      for (int s = lane; s < tsz; s += G) {
+        const int32_t key = keys[s];
+        if (key != -1) {
+          kmin = min(kmin, key);
+          kmax = max(kmax, key);
+        }
       }
-    }
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-      kmin = min(kmin, __shfl_xor_sync(gm, kmin, o, G));
-      kmax = max(kmax, __shfl_xor_sync(gm, kmax, o, G));
+      for (int o = G / 2; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(gm, kmin, o, G));
+        kmax = max(kmax, __shfl_xor_sync(gm, kmax, o, G));
+      }
     }
     const bool narrow = static_cast<unsigned>(kmax - kmin) < ((0xffffffffu >> lg) - 1u);
     int run = 0;
