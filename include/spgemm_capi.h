@@ -66,6 +66,9 @@ typedef struct spgemm_options {
   int32_t sym_launch_order[SPGEMM_NUM_BINS];
   int32_t has_num_launch_order;
   int32_t num_launch_order[SPGEMM_NUM_BINS];
+  int32_t ordered_heap;    /* B200 extension: 1 = heap-tier rows (numeric bin 7)
+                              fold in the reference's order (bitwise, slower);
+                              0 = bitmap rank + fp64 atomics (within 1e-12)   */
 } spgemm_options;
 
 /* StepTimings (pipeline.hpp:93-102), seconds, measured with CUDA events. */

@@ -31,7 +31,7 @@ class Options(C.Structure):
                 ("overlap", C.c_int32), ("deterministic", C.c_int32), ("chunk_rows", C.c_int64),
                 ("hash_scale", C.c_int64), ("has_sym_launch_order", C.c_int32),
                 ("sym_launch_order", C.c_int32 * NUM_BINS), ("has_num_launch_order", C.c_int32),
-                ("num_launch_order", C.c_int32 * NUM_BINS)]
+                ("num_launch_order", C.c_int32 * NUM_BINS), ("ordered_heap", C.c_int32)]
 
 
 class Timings(C.Structure):

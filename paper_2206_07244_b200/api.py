@@ -458,6 +458,9 @@ class SpgemmOptions:
     alloc_stats: Optional[AllocStats] = None
     sym_launch_order: Optional[Sequence[int]] = None
     num_launch_order: Optional[Sequence[int]] = None
+    # B200 extension: fold heap-tier rows (numeric bin 7) in the reference's
+    # order -- bitwise equal, slower; default: bitmap rank + fp64 atomics (1e-12)
+    ordered_heap: bool = False
 
     def _c(self) -> _c.Options:
         o = _c.Options()
@@ -469,6 +472,7 @@ class SpgemmOptions:
         o.deterministic = int(bool(self.deterministic))
         o.chunk_rows = int(self.chunk_rows)
         o.hash_scale = int(self.hash_scale)
+        o.ordered_heap = int(bool(self.ordered_heap))
         if self.sym_launch_order is not None:
             if len(self.sym_launch_order) != kNumBins:
                 raise InvalidArgument("launch order must be a permutation of the bin indices")

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "kernels_heap.cuh"
 #include "spgemm_capi.h"
 
 using namespace spgemm_b200;
@@ -370,6 +371,9 @@ struct spgemm_pipeline {
   void launch_num_bin(int bin, const RowList& rl, cudaStream_t s, int32_t* gkeys, double* gvals,
                       uint32_t* gbits, int64_t gslots, int64_t gwords, int gblocks);
   void release(bool keep_result);
+  // heap-tier numeric: bitmap + rank with fp64 atomics (default), or the
+  // ordered per-A-entry kernel (options.ordered_heap: bitwise summation order)
+  bool heap_bitmap() const { return idx32 && !opts.ordered_heap; }
 };
 
 namespace {
@@ -508,6 +512,15 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
                kern<<<grid, threads, smem, s>>>(rl, A, B, d_rpt, scale, d_spill, d_info_sym,
                                      static_cast<int>(sym_plan.strategies[bin].spill_threshold)));
   };
+  if (bin == kNumBins - 1 && idx32) {
+    // bitmap kernel: exact counts, no spill recount (kernels_heap.cuh)
+    prepare_kernel(ctx, k_big_sym, kBigSymSmem);
+    const int grid = persistent_grid(ctx, k_big_sym, kBigThreads, kBigSymSmem, rl.count);
+    SPG_LAUNCH(ctx, "k_big_sym", s,
+               k_big_sym<<<grid, kBigThreads, kBigSymSmem, s>>>(
+                   rl, A, B, d_rpt, d_info_sym, static_cast<int>(sym_plan.strategies[bin].spill_threshold)));
+    return;
+  }
   if (bin == kNumBins - 1) {
     block(k_sym_block<32768, 1024, true>, 32768, 1024);
     // Heap-tier recompute of the spilled rows (pipeline.cpp:315-348): a pool
@@ -672,7 +685,12 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     SPG_LAUNCH(ctx, "k_num_block<" + std::to_string(T) + ">", s,
                kern<<<grid, threads, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
   };
-  if (bin == kNumBins - 1 || u > 4096) {
+  if ((bin == kNumBins - 1 || u > 4096) && heap_bitmap()) {
+    prepare_kernel(ctx, k_big_num, kBigNumSmem);
+    const int grid = persistent_grid(ctx, k_big_num, kBigThreads, kBigNumSmem, rl.count);
+    SPG_LAUNCH(ctx, "k_big_num", s,
+               k_big_num<<<grid, kBigThreads, kBigNumSmem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, d_info_num));
+  } else if (bin == kNumBins - 1 || u > 4096) {
     SPG_LAUNCH(ctx, "k_num_global", s,
                k_num_global<<<gblocks, kGlobalThreads, 0, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, gkeys,
                                                     gvals, gbits, gslots, gwords, d_info_num));
@@ -714,7 +732,7 @@ void spgemm_pipeline::run_numeric() {
   uint32_t* gbits = nullptr;
   int64_t gslots = 0, gwords = 0;
   int gblocks = 0;
-  if (grows > 0) {
+  if (grows > 0 && !heap_bitmap()) {
     gslots = 2;
     while (gslots < 2 * h_num.max_metric) gslots <<= 1;
     gwords = std::min<int64_t>(int64_t(1) << 17, std::max<int64_t>(1, ceil_div(B.cols, 32)));

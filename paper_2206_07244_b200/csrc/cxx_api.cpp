@@ -366,6 +366,7 @@ SpgemmPipeline::SpgemmPipeline(const CsrMatrix& a, const CsrMatrix& b, const Spg
   o.deterministic = options.deterministic ? 1 : 0;
   o.chunk_rows = options.chunk_rows;
   o.hash_scale = options.hash.hash_scale;
+  o.ordered_heap = options.ordered_heap ? 1 : 0;
   if (options.sym_launch_order) {
     o.has_sym_launch_order = 1;
     std::copy(options.sym_launch_order->begin(), options.sym_launch_order->end(), o.sym_launch_order);

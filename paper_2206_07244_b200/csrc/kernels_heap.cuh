@@ -1,0 +1,248 @@
+// kernels_heap.cuh -- the heaviest rows: symbolic bin 7 and the numeric heap
+// tier (reference: the spill/heap paths, pipeline.cpp:315-348 and 396-410,
+// hash_tables.cpp:113-123), re-designed around a shared-memory BITMAP of the
+// output row's column set instead of a (global) hash table.
+//
+// One 1024-thread block per row, one block per SM (the bitmap takes 128 KB of
+// the SM's shared memory). Columns are handled in windows of 2^20 (one window
+// for every B with <= 1M columns).
+//
+//   symbolic   bit per product (atomicOr); the count is the number of bits the
+//              row set. Exact, no probing, no table size to outgrow, so the
+//              reference's spill recount is not needed -- the rows it would
+//              have spilled (count > 0.8 * 24575) are still counted and
+//              reported as spilled_rows.
+//   numeric    pass A sets the bits again; a rank directory (uint16 prefix per
+//              word within a 64-word superblock + uint32 superblock prefix)
+//              gives every column its output position, so C.col is written
+//              sorted straight from the bitmap (no comparison sort) and the
+//              products of pass B land at their position. Pass B adds with
+//              fp64 atomics into C.val (RED.ADD.F64): the result is within the
+//              north-star 1e-12 tolerance but the summation order is not the
+//              reference's. SpgemmOptions::ordered_heap selects the ordered
+//              (bitwise) heap kernel k_num_global instead.
+//
+// Work distribution ("flattened" products). A row's A entries are taken in
+// tiles of 1024; the tile's non-empty entries are compacted and prefix-summed
+// by B row length, and warp w takes the w-th 1/32 of the tile's products --
+// balanced however skewed the B rows are (R-MAT hubs). Within a warp, 32
+// consecutive products per round: lane l's entry is found with a 5-step
+// shuffle search over the next 32 entry starts.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace spgemm_b200 {
+
+constexpr int kBigThreads = 1024;
+constexpr int kBigWarps = kBigThreads / 32;
+constexpr int kBigWindowLog = 20;
+constexpr int64_t kBigWindow = int64_t(1) << kBigWindowLog;  // columns per bitmap window
+constexpr int kBigWords = static_cast<int>(kBigWindow / 32);  // 32768 words = 128 KB
+constexpr int kBigSuper = 64;                                  // words per rank superblock
+constexpr int kBigWordsPerThread = kBigWords / kBigThreads;    // 32
+
+// Staged tile of A entries (compacted: non-empty B rows only).
+struct BigTile {
+  long long S[kBigThreads + 1];  // product prefix; S[n] = tile total
+  int32_t b0[kBigThreads];       // B row start (32-bit index path)
+  double av[kBigThreads];        // A value
+  long long red[kBigWarps];
+};
+
+// The numeric kernel's bitmap and word prefixes are padded (one word / two
+// halfwords per 32) so the rank pass, where thread t scans words [32t, 32t+32),
+// is free of bank conflicts.
+constexpr int kBigWordsPad = kBigWords + kBigWords / 32;
+constexpr int kBigPrePad = kBigWords + 2 * (kBigWords / 32);
+__device__ __forceinline__ uint32_t bm_idx(uint32_t w) { return w + (w >> 5); }
+__device__ __forceinline__ uint32_t pre_idx(uint32_t w) { return w + 2 * (w >> 5); }
+
+constexpr size_t kBigSymSmem = sizeof(uint32_t) * kBigWords + sizeof(BigTile);
+constexpr size_t kBigNumSmem = sizeof(uint32_t) * kBigWordsPad + sizeof(uint16_t) * kBigPrePad +
+                               sizeof(uint32_t) * (kBigWords / kBigSuper) + sizeof(BigTile);
+static_assert(kBigNumSmem <= 227 * 1024, "heap-tier numeric block exceeds the opt-in shared memory");
+
+// Walks every product of A row [a0, a1): visit(col, x, valid) is called by all
+// 32 lanes of every warp once per round (valid = the lane holds a product).
+template <bool VALS, typename F>
+__device__ __forceinline__ void big_walk(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1, BigTile& t,
+                                         F visit) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t e0 = a0; e0 < a1; e0 += kBigThreads) {
+    const int ne = static_cast<int>(min(static_cast<int64_t>(kBigThreads), a1 - e0));
+    long long len = 0;
+    int32_t b0 = 0;
+    double av = 0.0;
+    if (tid < ne) {
+      const int32_t k = A.col[e0 + tid];
+      const int64_t r0 = B.rpt[k];
+      len = B.rpt[k + 1] - r0;
+      b0 = static_cast<int32_t>(r0);
+      if constexpr (VALS) av = A.val[e0 + tid];
+    }
+    // one scan gives both the compacted index (low 11 bits) and the product prefix
+    long long total;
+    const long long ex = block_exclusive_scan<kBigThreads>((len << 11) | (len > 0 ? 1 : 0), t.red, &total);
+    if (len > 0) {
+      const int ci = static_cast<int>(ex & 2047);
+      t.S[ci] = ex >> 11;
+      t.b0[ci] = b0;
+      t.av[ci] = av;
+    }
+    const int nce = static_cast<int>(total & 2047);
+    const long long P = total >> 11;
+    if (tid == 0) t.S[nce] = P;
+    __syncthreads();
+    const long long pw0 = P * warp / kBigWarps, pw1 = P * (warp + 1) / kBigWarps;
+    if (pw0 < pw1) {
+      // jc = the entry holding product pw0: largest j with S[j] <= pw0
+      int lo = 0, hi = nce - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (t.S[mid] <= pw0) lo = mid;
+        else hi = mid - 1;
+      }
+      int jc = lo;
+      for (long long p0 = pw0; p0 < pw1; p0 += 32) {
+        // d = start of entry jc+1+lane relative to p0 (strictly increasing, >= lane+1)
+        const int je = jc + 1 + lane;
+        const long long d = je <= nce ? t.S[je] - p0 : (1ll << 40);
+        int cnt = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const long long dm = __shfl_sync(kFull, d, cnt + step - 1);
+          if (dm <= lane) cnt += step;
+        }
+        const long long p = p0 + lane;
+        const bool valid = p < pw1;
+        const int j = jc + cnt;
+        int32_t col = -1;
+        double x = 0.0;
+        if (valid) {
+          const int32_t at = t.b0[j] + static_cast<int32_t>(p - t.S[j]);
+          col = B.col[at];
+          if constexpr (VALS) x = __dmul_rn(t.av[j], B.val[at]);
+        }
+        visit(col, x, valid);
+        // next round starts at p0+32: the entry holding it (one more if an
+        // entry starts exactly there)
+        jc += __shfl_sync(kFull, cnt, 31);
+        if (jc + 1 <= nce && t.S[jc + 1] == p0 + 32) ++jc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Symbolic, bin 7: rl lists the rows; the count of row i replaces its nprod
+// in rpt. Rows counting more than `thresh` (the reference's spill threshold)
+// are counted in info->spill_count.
+__global__ void __launch_bounds__(kBigThreads, 1)
+    k_big_sym(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, DevInfo* info, int thresh) {
+  const RowList rl = rl_in.resolved();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
+  BigTile& t = *reinterpret_cast<BigTile*>(smem_raw + sizeof(uint32_t) * kBigWords);
+  const int tid = threadIdx.x;
+  for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
+    const int64_t row = rl.row(idx);
+    if (rpt[row] == 0) continue;  // no products (pipeline.cpp:368-371)
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    long long cnt = 0;
+    for (int64_t wc0 = 0; wc0 < B.cols; wc0 += kBigWindow) {
+      const int nwords = static_cast<int>((min(kBigWindow, B.cols - wc0) + 31) >> 5);
+      uint4* b4 = reinterpret_cast<uint4*>(bm);
+      for (int s = tid; s < (nwords + 3) >> 2; s += kBigThreads) b4[s] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+      const int32_t c0 = static_cast<int32_t>(wc0);
+      big_walk<false>(A, B, a0, a1, t, [&](int32_t col, double, bool valid) {
+        const uint32_t off = static_cast<uint32_t>(col - c0);
+        if (valid && off < static_cast<uint32_t>(kBigWindow)) {
+          const uint32_t bit = 1u << (off & 31u);  // (symbolic: unpadded bitmap)
+          cnt += (atomicOr(bm + (off >> 5), bit) & bit) == 0u;
+        }
+      });
+    }
+    const long long total = block_sum_ll<kBigThreads>(cnt, t.red);
+    if (tid == 0) {
+      rpt[row] = total;
+      if (total > thresh) atomicAdd(&info->spill_count, 1ull);
+    }
+    __syncthreads();
+  }
+}
+
+// Numeric heap tier (see the header comment).
+__global__ void __launch_bounds__(kBigThreads, 1)
+    k_big_num(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
+              double* __restrict__ cval, DevInfo* info) {
+  const RowList rl = rl_in.resolved();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
+  uint16_t* pre = reinterpret_cast<uint16_t*>(smem_raw + sizeof(uint32_t) * kBigWordsPad);
+  uint32_t* sup =
+      reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint32_t) * kBigWordsPad + sizeof(uint16_t) * kBigPrePad);
+  BigTile& t = *reinterpret_cast<BigTile*>(smem_raw + sizeof(uint32_t) * kBigWordsPad +
+                                           sizeof(uint16_t) * kBigPrePad + sizeof(uint32_t) * (kBigWords / kBigSuper));
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
+    const int64_t row = rl.row(idx);
+    const int64_t base = rpt[row];
+    const int64_t n = rpt[row + 1] - base;
+    if (n == 0) continue;
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    int64_t woff = 0;  // entries of the row in earlier windows
+    for (int64_t wc0 = 0; wc0 < B.cols; wc0 += kBigWindow) {
+      uint4* b4 = reinterpret_cast<uint4*>(bm);  // whole (padded) bitmap: the rank pass reads all of it
+      for (int s = tid; s < kBigWordsPad / 4; s += kBigThreads) b4[s] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+      const int32_t c0 = static_cast<int32_t>(wc0);
+      // ---- pass A: the window's column set
+      big_walk<false>(A, B, a0, a1, t, [&](int32_t col, double, bool valid) {
+        const uint32_t off = static_cast<uint32_t>(col - c0);
+        if (valid && off < static_cast<uint32_t>(kBigWindow)) atomicOr(bm + bm_idx(off >> 5), 1u << (off & 31u));
+      });
+      // ---- rank directory; C.col written from the bitmap, C.val zeroed
+      const int w0 = tid * kBigWordsPerThread;  // 32 words: half a superblock
+      int mine = 0;
+#pragma unroll 8
+      for (int i = 0; i < kBigWordsPerThread; ++i) mine += __popc(bm[bm_idx(w0 + i)]);
+      long long wtot;
+      const long long g = block_exclusive_scan<kBigThreads>(mine, t.red, &wtot);
+      const long long sbase = __shfl_sync(kFull, g, lane & ~1);  // prefix before the superblock
+      if ((tid & 1) == 0) sup[tid >> 1] = static_cast<uint32_t>(g);
+      int run = static_cast<int>(g - sbase);
+      int64_t pos = woff + g;
+      for (int i = 0; i < kBigWordsPerThread; ++i) {
+        const int w = w0 + i;
+        uint32_t m = bm[bm_idx(w)];
+        pre[pre_idx(w)] = static_cast<uint16_t>(run);
+        run += __popc(m);
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1u;
+          ccol[base + pos] = c0 + w * 32 + b;
+          cval[base + pos] = 0.0;
+          ++pos;
+        }
+      }
+      __syncthreads();  // rank directory + zeroed C.val visible to the block
+      // ---- pass B: products accumulate at their rank
+      double* crow = cval + base + woff;
+      big_walk<true>(A, B, a0, a1, t, [&](int32_t col, double x, bool valid) {
+        const uint32_t off = static_cast<uint32_t>(col - c0);
+        if (valid && off < static_cast<uint32_t>(kBigWindow)) {
+          const uint32_t w = off >> 5;
+          const uint32_t r = sup[w / kBigSuper] + pre[pre_idx(w)] + __popc(bm[bm_idx(w)] & ((1u << (off & 31u)) - 1u));
+          atomicAdd(crow + r, x);
+        }
+      });
+      woff += wtot;
+    }
+    if (tid == 0 && woff != n) atomicOr(&info->error, kErrNumericCount);
+    __syncthreads();
+  }
+}
+
+}  // namespace spgemm_b200

@@ -69,14 +69,25 @@ def bitwise_equal(x: CsrMatrix, y) -> bool:
             and np.array_equal(np.asarray(x.val).view(np.int64), np.asarray(y.val).view(np.int64)))
 
 
-def assert_matches_oracle(out_c: CsrMatrix, expected, tol: float = 1e-12, bitwise: bool = True):
-    """Structure bit-exact; values bitwise (deterministic ordered fold) and within tol."""
+HEAP_NNZ = 4096  # rows above this (num_2x bin 7) take the heap tier: fp64 atomics unless ordered_heap
+
+
+def assert_matches_oracle(out_c: CsrMatrix, expected, tol: float = 1e-12, bitwise=None):
+    """Structure bit-exact; values within tol everywhere and bitwise (the reference's
+    summation order) on every row outside the numeric heap tier -- on all rows when
+    bitwise=True (ordered_heap=True runs), on none when bitwise=False."""
     from oracle import oracle as O
     c = out_c.to_host()
     assert c.rows == expected.rows and c.cols == expected.cols
     assert np.array_equal(c.rpt, expected.rpt), "row pointers differ"
     assert np.array_equal(c.col, expected.col), "column indices differ"
     assert O.max_relative_error(c, expected) <= tol
-    if bitwise:
-        assert np.array_equal(c.val.view(np.int64), np.asarray(expected.val).view(np.int64)), \
-            "values differ bitwise from the reference's summation order"
+    if bitwise is False:
+        return
+    got = np.asarray(c.val).view(np.int64)
+    exp = np.asarray(expected.val).view(np.int64)
+    if bitwise is None:
+        lens = np.diff(np.asarray(expected.rpt))
+        keep = np.repeat(lens <= HEAP_NNZ, lens)
+        got, exp = got[keep], exp[keep]
+    assert np.array_equal(got, exp), "values differ bitwise from the reference's summation order"

@@ -177,6 +177,15 @@ def test_spill_to_global_tier(sg, oracle):  # :285-296
     assert out.c.row_nnz(0) == 20000
 
 
+@pytest.mark.parametrize("pair", [(20000, 200), (6000, 60)])
+def test_heap_tier_ordered_is_bitwise(sg, oracle, pair):
+    """ordered_heap=True: heap-tier rows fold in the reference's order (bitwise)."""
+    a, b = spill_pair(*pair)
+    a, b = S.random_values(a, 5), S.random_values(b, 6)
+    out = sg.multiply(a, b, sg.SpgemmOptions(ordered_heap=True))
+    assert_matches_oracle(out.c, oracle.spgemm(a, b), bitwise=True)
+
+
 def test_spill_threshold_stays_fixed(sg):  # :298-303
     a, b = spill_pair(19660, 20)
     out = sg.multiply(a, b)

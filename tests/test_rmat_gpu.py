@@ -64,8 +64,12 @@ class _CAI:
 
 def test_rmat16_full_oracle(sg, oracle):
     a = S.random_values(S.rmat(16, 16, seed=16), 1)
+    exp = oracle.spgemm(a, a)
+    assert (np.diff(exp.rpt) > 4096).any(), "the case must reach the numeric heap tier"
     out = sg.multiply(a, a)
-    assert_matches_oracle(out.c, oracle.spgemm(a, a))
+    assert_matches_oracle(out.c, exp)  # bitwise outside the heap tier, 1e-12 inside
+    out = sg.multiply(a, a, sg.SpgemmOptions(ordered_heap=True))
+    assert_matches_oracle(out.c, exp, bitwise=True)
 
 
 @pytest.mark.slow
