@@ -42,12 +42,15 @@ constexpr int kBigWords = static_cast<int>(kBigWindow / 32);  // 32768 words = 1
 constexpr int kBigSuper = 64;                                  // words per rank superblock
 constexpr int kBigWordsPerThread = kBigWords / kBigThreads;    // 32
 
-// Staged tile of A entries (compacted: non-empty B rows only).
+// Staged tile of A entries (compacted: non-empty B rows only). Product
+// offsets within a tile are 32-bit: a tile takes at most 1024 entries and
+// stops early before its product count would reach 2^31.
 struct BigTile {
-  long long S[kBigThreads + 1];  // product prefix; S[n] = tile total
-  int32_t b0[kBigThreads];       // B row start (32-bit index path)
-  double av[kBigThreads];        // A value
+  int32_t S[kBigThreads + 1];  // product prefix; S[n] = tile total
+  int32_t b0[kBigThreads];     // B row start (32-bit index path)
+  double av[kBigThreads];      // A value
   long long red[kBigWarps];
+  int nce, ne;                 // compacted entries, A entries consumed
 };
 
 // The numeric kernel's bitmap and word prefixes are padded (one word / two
@@ -65,11 +68,15 @@ static_assert(kBigNumSmem <= 227 * 1024, "heap-tier numeric block exceeds the op
 
 // Walks every product of A row [a0, a1): visit(col, x, valid) is called by all
 // 32 lanes of every warp once per round (valid = the lane holds a product).
+// Round mapping: lane l of a round starting at product p0 belongs to entry
+// jc + popc(M & bits<=l), where jc holds p0 and M has bit d set for every
+// entry starting at p0+d (d in 1..31) -- one REDUX.OR per 32 products.
 template <bool VALS, typename F>
 __device__ __forceinline__ void big_walk(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1, BigTile& t,
                                          F visit) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t e0 = a0; e0 < a1; e0 += kBigThreads) {
+  constexpr long long kLimit = (1ll << 31) - 1;
+  for (int64_t e0 = a0; e0 < a1; e0 += t.ne) {
     const int ne = static_cast<int>(min(static_cast<int64_t>(kBigThreads), a1 - e0));
     long long len = 0;
     int32_t b0 = 0;
@@ -84,17 +91,25 @@ __device__ __forceinline__ void big_walk(const DevCsr& A, const DevCsr& B, int64
     // one scan gives both the compacted index (low 11 bits) and the product prefix
     long long total;
     const long long ex = block_exclusive_scan<kBigThreads>((len << 11) | (len > 0 ? 1 : 0), t.red, &total);
-    if (len > 0) {
-      const int ci = static_cast<int>(ex & 2047);
-      t.S[ci] = ex >> 11;
+    const long long s64 = ex >> 11;
+    const bool in = tid < ne && s64 + len <= kLimit;  // a prefix of the tile's entries
+    const int ne_eff = __syncthreads_count(in);
+    const int ci = static_cast<int>(ex & 2047);
+    if (in && len > 0) {
+      t.S[ci] = static_cast<int32_t>(s64);
       t.b0[ci] = b0;
       t.av[ci] = av;
     }
-    const int nce = static_cast<int>(total & 2047);
-    const long long P = total >> 11;
-    if (tid == 0) t.S[nce] = P;
+    if (tid == ne_eff - 1) {
+      t.nce = ci + (len > 0 ? 1 : 0);
+      t.S[t.nce] = static_cast<int32_t>(s64 + len);
+      t.ne = ne_eff;
+    }
     __syncthreads();
-    const long long pw0 = P * warp / kBigWarps, pw1 = P * (warp + 1) / kBigWarps;
+    const int nce = t.nce;
+    const int P = t.S[nce];
+    const int pw0 = static_cast<int>(static_cast<long long>(P) * warp / kBigWarps);
+    const int pw1 = static_cast<int>(static_cast<long long>(P) * (warp + 1) / kBigWarps);
     if (pw0 < pw1) {
       // jc = the entry holding product pw0: largest j with S[j] <= pw0
       int lo = 0, hi = nce - 1;
@@ -104,31 +119,56 @@ __device__ __forceinline__ void big_walk(const DevCsr& A, const DevCsr& B, int64
         else hi = mid - 1;
       }
       int jc = lo;
-      for (long long p0 = pw0; p0 < pw1; p0 += 32) {
-        // d = start of entry jc+1+lane relative to p0 (strictly increasing, >= lane+1)
-        const int je = jc + 1 + lane;
-        const long long d = je <= nce ? t.S[je] - p0 : (1ll << 40);
-        int cnt = 0;
+      int p0 = pw0;
+      while (p0 < pw1) {
+        // Long run: the next >= 32 products all belong to entry jc (most of the
+        // product mass of skewed matrices comes from long B rows) -- no entry
+        // search, U rounds of loads in flight.
+        const int send = t.S[jc + 1];
+        if (send - p0 >= 32) {
+          const int stop = min(send, pw1);
+          const int32_t bj = t.b0[jc] - t.S[jc];
+          const double a = VALS ? t.av[jc] : 0.0;
+          constexpr int U = 4;
+          for (; p0 + 32 * U <= stop; p0 += 32 * U) {
+            int32_t c[U];
+            double bv[U];
 #pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const long long dm = __shfl_sync(kFull, d, cnt + step - 1);
-          if (dm <= lane) cnt += step;
+            for (int u = 0; u < U; ++u) {
+              c[u] = B.col[bj + p0 + 32 * u + lane];
+              if constexpr (VALS) bv[u] = B.val[bj + p0 + 32 * u + lane];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) visit(c[u], VALS ? __dmul_rn(a, bv[u]) : 0.0, true);
+          }
+          for (; p0 + 32 <= stop; p0 += 32) {
+            const int32_t at = bj + p0 + lane;
+            visit(B.col[at], VALS ? __dmul_rn(a, B.val[at]) : 0.0, true);
+          }
+          if (p0 >= pw1) break;
+          if (p0 == send) {
+            ++jc;
+            continue;
+          }
         }
-        const long long p = p0 + lane;
+        // General round: lane l belongs to entry jc + popc(M & bits<=l).
+        const int je = jc + 1 + lane;
+        const int d = je <= nce ? t.S[je] - p0 : 64;  // >= lane + 1
+        const unsigned M = __reduce_or_sync(kFull, d < 32 ? (1u << d) : 0u);
+        const int j = jc + __popc(M & ((2u << lane) - 1u));
+        const int p = p0 + lane;
         const bool valid = p < pw1;
-        const int j = jc + cnt;
         int32_t col = -1;
         double x = 0.0;
         if (valid) {
-          const int32_t at = t.b0[j] + static_cast<int32_t>(p - t.S[j]);
+          const int32_t at = t.b0[j] + (p - t.S[j]);
           col = B.col[at];
           if constexpr (VALS) x = __dmul_rn(t.av[j], B.val[at]);
         }
         visit(col, x, valid);
-        // next round starts at p0+32: the entry holding it (one more if an
-        // entry starts exactly there)
-        jc += __shfl_sync(kFull, cnt, 31);
-        if (jc + 1 <= nce && t.S[jc + 1] == p0 + 32) ++jc;
+        // next round starts at p0+32: the entry holding it
+        jc += __popc(M) + (__any_sync(kFull, d == 32) ? 1 : 0);
+        p0 += 32;
       }
     }
     __syncthreads();
@@ -213,20 +253,30 @@ __global__ void __launch_bounds__(kBigThreads, 1)
       const long long sbase = __shfl_sync(kFull, g, lane & ~1);  // prefix before the superblock
       if ((tid & 1) == 0) sup[tid >> 1] = static_cast<uint32_t>(g);
       int run = static_cast<int>(g - sbase);
-      int64_t pos = woff + g;
       for (int i = 0; i < kBigWordsPerThread; ++i) {
         const int w = w0 + i;
-        uint32_t m = bm[bm_idx(w)];
         pre[pre_idx(w)] = static_cast<uint16_t>(run);
-        run += __popc(m);
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1u;
-          ccol[base + pos] = c0 + w * 32 + b;
-          cval[base + pos] = 0.0;
-          ++pos;
+        run += __popc(bm[bm_idx(w)]);
+      }
+      __syncthreads();
+      // C.col straight from the bitmap, word-major (consecutive threads take
+      // consecutive words, so a warp's stores cover one contiguous span);
+      // C.val of the window zeroed with coalesced stores.
+      for (int w = tid; w < kBigWords; w += kBigThreads) {
+        uint32_t m = bm[bm_idx(w)];
+        if (m) {
+          int64_t pos = woff + sup[w / kBigSuper] + pre[pre_idx(w)];
+          do {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+#ifndef SPGEMM_ABLATE_OUT  // diagnostic builds only (tools/build_ablation.sh)
+            ccol[base + pos] = c0 + w * 32 + b;
+#endif
+            ++pos;
+          } while (m);
         }
       }
+      for (int64_t e = tid; e < wtot; e += kBigThreads) cval[base + woff + e] = 0.0;
       __syncthreads();  // rank directory + zeroed C.val visible to the block
       // ---- pass B: products accumulate at their rank
       double* crow = cval + base + woff;
@@ -235,7 +285,11 @@ __global__ void __launch_bounds__(kBigThreads, 1)
         if (valid && off < static_cast<uint32_t>(kBigWindow)) {
           const uint32_t w = off >> 5;
           const uint32_t r = sup[w / kBigSuper] + pre[pre_idx(w)] + __popc(bm[bm_idx(w)] & ((1u << (off & 31u)) - 1u));
+#ifndef SPGEMM_ABLATE_RED
           atomicAdd(crow + r, x);
+#else
+          if (x == 1.2345e-300) crow[r] = x;
+#endif
         }
       });
       woff += wtot;
