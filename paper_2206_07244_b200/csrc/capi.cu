@@ -512,13 +512,18 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
                kern<<<grid, threads, smem, s>>>(rl, A, B, d_rpt, scale, d_spill, d_info_sym,
                                      static_cast<int>(sym_plan.strategies[bin].spill_threshold)));
   };
-  if (bin == kNumBins - 1 && idx32) {
+  // Bitmap kernel for the top bin, and for the block-table bins too when the
+  // rows' B rows are short on average (skewed graphs: a per-A-entry table walk
+  // leaves most lanes idle there; the bitmap walk is balanced by products).
+  if (idx32 && (bin == kNumBins - 1 || (u > 2048 && avg_b_len < 64.0))) {
     // bitmap kernel: exact counts, no spill recount (kernels_heap.cuh)
     prepare_kernel(ctx, k_big_sym, kBigSymSmem);
     const int grid = persistent_grid(ctx, k_big_sym, kBigThreads, kBigSymSmem, rl.count);
     SPG_LAUNCH(ctx, "k_big_sym", s,
                k_big_sym<<<grid, kBigThreads, kBigSymSmem, s>>>(
-                   rl, A, B, d_rpt, d_info_sym, static_cast<int>(sym_plan.strategies[bin].spill_threshold)));
+                   rl, A, B, d_rpt, d_info_sym,
+                   bin == kNumBins - 1 ? static_cast<int>(sym_plan.strategies[bin].spill_threshold)
+                                       : std::numeric_limits<int>::max()));
     return;
   }
   if (bin == kNumBins - 1) {

@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
       __syncthreads();  // rank directory + zeroed C.val visible to the block
       // ---- pass B: products accumulate at their rank
       double* crow = cval + base + woff;
+#ifndef SPGEMM_ABLATE_PASSB
       big_walk<true>(A, B, a0, a1, t, [&](int32_t col, double x, bool valid) {
         const uint32_t off = static_cast<uint32_t>(col - c0);
         if (valid && off < static_cast<uint32_t>(kBigWindow)) {
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
 #endif
         }
       });
+#endif
       woff += wtot;
     }
     if (tid == 0 && woff != n) atomicOr(&info->error, kErrNumericCount);
