@@ -573,6 +573,20 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+// Row order of the persistent group kernels: block b takes the contiguous
+// index range [b*per, (b+1)*per) of its bin and its NGRP groups interleave
+// inside it, so co-resident groups work on adjacent rows (shared B rows hit
+// in L1) and each block walks its range in order (temporal locality).
+struct BlockRange {
+  int64_t begin, end;
+  __device__ __forceinline__ BlockRange(int64_t count, int ngrp) {
+    int64_t per = (count + gridDim.x - 1) / gridDim.x;
+    per = (per + ngrp - 1) / ngrp * ngrp;
+    begin = min(count, static_cast<int64_t>(blockIdx.x) * per);
+    end = min(count, begin + per);
+  }
+};
+
 // ------------------------------------------------------------- row walker
 template <int G>
 __device__ __forceinline__ int group_max(int v, unsigned gm) {
@@ -880,9 +894,14 @@ __global__ void __launch_bounds__(G* NGRP)
                     (threadIdx.x / G) * G;
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
+#ifdef SPGEMM_ABLATE_STRIDED
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NGRP;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * NGRP + threadIdx.x / G; idx < rl.count;
        idx += stride) {
+#else
+  const BlockRange br(rl.count, NGRP);
+  for (int64_t idx = br.begin + threadIdx.x / G; idx < br.end; idx += NGRP) {
+#endif
     const int64_t row = rl.row(idx);
     const long long np = rpt[row];
     if (np == 0) continue;  // no products: nnz 0 (pipeline.cpp:368-371)
@@ -944,7 +963,12 @@ __global__ void __launch_bounds__(256)
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + warp * TS * 32 + lane;
   const Hash hs = make_hash(scale, log2_const<TS>());
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+#ifdef SPGEMM_ABLATE_STRIDED
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rl.count; idx += stride) {
+#else
+  const BlockRange br(rl.count, blockDim.x);
+  for (int64_t idx = br.begin + threadIdx.x; idx < br.end; idx += blockDim.x) {
+#endif
     const int64_t row = rl.row(idx);
     if (rpt[row] == 0) continue;
 #pragma unroll
@@ -989,7 +1013,12 @@ __global__ void __launch_bounds__(128)
                   warp * TS * 32 + lane;
   const Hash hs = make_hash(scale, log2_const<TS>());
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+#ifdef SPGEMM_ABLATE_STRIDED
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rl.count; idx += stride) {
+#else
+  const BlockRange br(rl.count, blockDim.x);
+  for (int64_t idx = br.begin + threadIdx.x; idx < br.end; idx += blockDim.x) {
+#endif
     const int64_t row = rl.row(idx);
     const int64_t base = rpt[row];
     const int n = static_cast<int>(rpt[row + 1] - base);
@@ -1232,8 +1261,10 @@ __device__ __forceinline__ void group_sort_inplace(K* buf, int n, int lane, unsi
 // column (hash_tables.cpp:137-177) and a coalesced write of C(i,:) at rpt[i].
 // The sort key packs (col - min col) with the slot index into 32 bits when the
 // row's column span allows (64 bits otherwise).
+// The 32x256 instance (3-D stencil rows) is latency-bound: capping it at 51
+// registers (5 resident blocks, 40 warps/SM) measured 3% faster than 64.
 template <int G, int T, int E, int NGRP, typename IT>
-__global__ void __launch_bounds__(G* NGRP)
+__global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
     k_num_group(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
                 DevInfo* info) {
@@ -1253,8 +1284,13 @@ __global__ void __launch_bounds__(G* NGRP)
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const unsigned gshift = (threadIdx.x & 31u) & ~(G - 1u);
+#ifdef SPGEMM_ABLATE_STRIDED
   const int64_t stride = static_cast<int64_t>(gridDim.x) * NGRP;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * NGRP + grp; idx < rl.count; idx += stride) {
+#else
+  const BlockRange br(rl.count, NGRP);
+  for (int64_t idx = br.begin + grp; idx < br.end; idx += NGRP) {
+#endif
     const int64_t row = rl.row(idx);
     const int64_t base = rpt[row];
     const int n = static_cast<int>(rpt[row + 1] - base);
