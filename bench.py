@@ -37,6 +37,7 @@ CONFIG_NAMES = {
     2: "C=A*A 3D 27-pt stencil 128^3",
     3: "C=A*A R-MAT scale 20 ef 16",
     4: "RAP: A*P then R*(AP), 3D 7-pt Poisson 128^3, trilinear P",
+    5: "C=A*A R-MAT scale 24 ef 16, row blocks x 2^20-column windows, C streamed to checksums",
 }
 
 
@@ -163,9 +164,13 @@ def run_reference(args):
         return
     from oracle import oracle as O
     from paper_2206_07244_b200.api import CsrMatrix
-    mats = build_workload(args.config)
+    if args.config == 5:
+        from paper_2206_07244_b200 import synthetic as S
+        mats = [S.rmat(args.rmat_scale, 16, seed=args.rmat_scale)] * 2
+    else:
+        mats = build_workload(args.config)
     a = mats[0]
-    frac = {1: 1.0, 2: 0.25, 3: 0.02, 4: 1.0}[args.config]
+    frac = {1: 1.0, 2: 0.25, 3: 0.02, 4: 1.0, 5: 0.0005}[args.config]
     r0 = int(a.rows * (0.5 - frac / 2)) if frac < 1 else 0
     r1 = r0 + int(a.rows * frac) if frac < 1 else a.rows
     rpt = a.rpt[r0:r1 + 1] - a.rpt[r0]
@@ -192,7 +197,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIG_NAMES[args.config], "sample_rows": [r0, r1]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"rows [{r0},{r1}) of config {args.config}'s A times B per step"},
@@ -206,13 +212,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--rmat-scale", type=int, default=24, help="config 5's R-MAT scale (24 = BASELINE)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 5:
+        return run_config5(args)
 
     import torch
     import paper_2206_07244_b200 as sg
@@ -468,10 +477,132 @@ def main():
         dist.destroy_process_group()
 
 
+def run_config5(args):
+    """BASELINE config 5: R-MAT scale 24, C = A*A, nprod ~1e12 and a
+    TB-scale C. Rows are split over the ranks by the nprod prefix (B broadcast once
+    over NCCL); each rank streams its rows through row-block x column-window tiles
+    (paper_2206_07244_b200/tiled.py), every tile a full device pipeline whose C is
+    reduced to checksums and freed. Strong scaling: the product is fixed."""
+    import torch
+    import paper_2206_07244_b200 as sg
+    from paper_2206_07244_b200 import synthetic as S
+    from paper_2206_07244_b200 import tiled as T
+    from paper_2206_07244_b200.distributed import broadcast_csr, nprod_split
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(os.environ.get("SPGEMM_DIST_BACKEND", "nccl"),
+                                device_id=torch.device("cuda", local))
+    ctx = sg.get_context(local)
+    t0 = time.perf_counter()
+    a_host = S.rmat(args.rmat_scale, 16, seed=args.rmat_scale) if rank == 0 else None
+    gen_s = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if dist:
+        dist.barrier()
+        B = broadcast_csr(a_host.to_device(local) if rank == 0 else None, 0, torch.device("cuda", local))
+    else:
+        B = a_host.to_device(local)
+    torch.cuda.synchronize()
+    bcast_s = time.perf_counter() - t0
+    nprod, total = sg.compute_nprod(B, B, device=local)
+    bounds = nprod_split(nprod, world)
+    rows = range(bounds[rank], bounds[rank + 1])
+    t0 = time.perf_counter()
+    wins = T.split_columns(B)
+    torch.cuda.synchronize()
+    split_s = time.perf_counter() - t0
+    budget = int(os.environ.get("SPGEMM_TILE_BUDGET", 12_000_000_000))
+
+    def step():
+        return T.stream_multiply(B, B, rows=rows, nprod=nprod, b_windows=wins, budget=budget, device=local)
+
+    for _ in range(max(3, args.warmup)):
+        rep = step()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if rank == 0:
+        clocks.start()
+    tw0 = time.time()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches0 = ctx.kernel_launches
+    nprod_done = 0
+    for _ in range(args.steps):
+        rep = step()
+        nprod_done += rep.total_nprod
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    if rank == 0:
+        clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    launches = ctx.kernel_launches - launches0
+    if dist:
+        dist.barrier()
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        nn = torch.tensor([nprod_done, rep.nnz], dtype=torch.int64, device="cuda")
+        dist.all_reduce(nn)
+        nprod_done, nnz_all = (int(x) for x in nn.tolist())
+    else:
+        nnz_all = rep.nnz
+    if rank == 0:
+        value = 2 * nprod_done / (t_ms * 1e-3) / 1e9
+        ms = t_ms / args.steps
+        # algorithmic bytes per step: A + B + C, C counted once as streamed through HBM
+        a_nnz = B.nnz()
+        step_bytes = 2 * csr_bytes(B.rows, a_nnz) + csr_bytes(B.rows, nnz_all)
+        peak, peak_kind = load_peaks()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[5], "rmat_scale": args.rmat_scale, "nprod_per_step": total,
+                       "nnz_c": nnz_all, "tiles_per_step_rank0": rep.tiles, "window_cols": T.WINDOW,
+                       "tile_budget_nprod": budget, "parallelism": f"row-block dp{world}",
+                       "l2": "inputs larger than L2", "generate_s": round(gen_s, 1),
+                       "b_broadcast_s": round(bcast_s, 3), "b_split_s": round(split_s, 3)},
+            "roofline": None,
+            "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9,
+                              "frac": step_bytes / (ms * 1e-3) / 1e9 / peak, "peak": peak, "peak_source": peak_kind},
+            "cpu_baseline": None,
+            "e2e": {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "note": "C is TB-scale: streamed to checksums on the device, never copied to the host"},
+            "checksums": {"nnz": nnz_all, "val_sum_rank0": rep.val_sum, "pattern_hash_rank0": rep.pattern_hash},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(tw0, tw1),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(a_host, rows_frac=0.0005, runs=1)
+                line["cpu_baseline"] = cpu
+            except Exception as e:  # pragma: no cover
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
+                                        "sample": str(e)}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_e2e(sg, torch, a_host, steps, device):
-    """Same metric through the public API with host buffers: each step copies A
-    from pinned host memory (B aliases A), multiplies, and reads C back into
-    pinned host buffers."""
+    """Same metric through the public API with host buffers: each step copies A from
+    pinned host memory (B aliases A), multiplies, and reads C back into pinned host
+    buffers. Pipelined like an application issuing independent products back to
+    back: step i's C download (DeviceMatrix.download_async, the context's copy lane)
+    overlaps step i+1's H2D and kernels; the timed region ends when every download
+    has landed. The fully synchronous variant (download inside the step) is reported
+    alongside as sync_value."""
     from paper_2206_07244_b200.api import CsrMatrix
     pr = torch.from_numpy(a_host.rpt).pin_memory()
     pc = torch.from_numpy(a_host.col).pin_memory()
@@ -487,8 +618,17 @@ def run_e2e(sg, torch, a_host, steps, device):
     ocol = torch.empty(nnz, dtype=torch.int32).pin_memory()
     oval = torch.empty(nnz, dtype=torch.float64).pin_memory()
     d2h = orpt.numel() * 8 + ocol.numel() * 4 + oval.numel() * 8
+    ctx = sg.get_context(device)
 
-    def step():
+    def step_pipelined():
+        p = sg.SpgemmPipeline(a, a, device=device)
+        dm, out = p.run_device()
+        p.close()
+        dm.download_async(orpt.numpy(), ocol.numpy(), oval.numpy(), release=True)
+        dm.free()
+        return out.stats.total_nprod
+
+    def step_sync():
         p = sg.SpgemmPipeline(a, a, device=device)
         dm, out = p.run_device()
         p.close()
@@ -496,15 +636,23 @@ def run_e2e(sg, torch, a_host, steps, device):
         dm.free()
         return out.stats.total_nprod
 
-    step()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    nprod = 0
-    for _ in range(steps):
-        nprod += step()
-    t = time.perf_counter() - t0
+    def timed(step):
+        step()
+        ctx.wait_downloads()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nprod = 0
+        for _ in range(steps):
+            nprod += step()
+        ctx.wait_downloads()
+        torch.cuda.synchronize()
+        return nprod, time.perf_counter() - t0
+
+    nprod, t = timed(step_pipelined)
+    nprod_s, t_s = timed(step_sync)
     return {"value": 2 * nprod / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": steps, "ms_per_step": t / steps * 1e3}
+            "steps": steps, "ms_per_step": t / steps * 1e3, "mode": "pipelined (download_async)",
+            "sync_value": 2 * nprod_s / t_s / 1e9, "sync_ms_per_step": t_s / steps * 1e3}
 
 
 if __name__ == "__main__":

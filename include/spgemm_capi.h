@@ -196,6 +196,20 @@ void spgemm_matrix_device_ptrs(const spgemm_matrix* m, const int64_t** rpt, cons
 spgemm_status spgemm_matrix_download(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t* rpt,
                                      int32_t* col, double* val);
 void spgemm_matrix_free(spgemm_matrix* m);
+/* B200 extension: stream-ordered D2H of C on the context's copy lane. Returns
+ * at once; the copy starts when the work already queued on the context's
+ * stream (the product) is done, so it overlaps the NEXT product's H2D and
+ * kernels. release != 0 frees C's device buffers behind the copy (the handle
+ * stays valid for spgemm_matrix_shape/_free). Host buffers should be pinned;
+ * they must stay untouched until spgemm_ctx_wait_downloads() returns. */
+spgemm_status spgemm_matrix_download_async(spgemm_ctx* ctx, spgemm_matrix* m, int64_t* rpt, int32_t* col,
+                                           double* val, int32_t release);
+spgemm_status spgemm_ctx_wait_downloads(spgemm_ctx* ctx);
+/* B200 extension (streamed products, tiled.py): checksums of C on the device --
+ * nnz, the sum of the values, and sum over entries of (col + col_offset + 1) *
+ * (row + row_offset + 1) mod 2^64 -- without copying C to the host. */
+spgemm_status spgemm_matrix_checksum(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t row_offset,
+                                     int64_t col_offset, double* val_sum, uint64_t* pattern_hash);
 
 /* ----------------------------------------------- standalone GPU kernels */
 /* compute_nprod() (reference.cpp:37-55) on the device: out[M] host or device. */

@@ -122,6 +122,9 @@ _decl("spgemm_matrix_shape", None, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int6
 _decl("spgemm_matrix_device_ptrs", None, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)])
 _decl("spgemm_matrix_download", _st, [_P, _P, _P, _P, _P])
 _decl("spgemm_matrix_free", None, [_P])
+_decl("spgemm_matrix_checksum", _st, [_P, _P, C.c_int64, C.c_int64, _P, _P])
+_decl("spgemm_matrix_download_async", _st, [_P, _P, _P, _P, _P, C.c_int32])
+_decl("spgemm_ctx_wait_downloads", _st, [_P])
 _decl("spgemm_compute_nprod", _st, [_P, C.POINTER(CsrView), C.POINTER(CsrView), _P, C.POINTER(C.c_int64)])
 _decl("spgemm_build_rpt", _st, [_P, _P, C.c_int64, C.POINTER(C.c_int64)])
 _decl("spgemm_run_binning", _st, [_P, _P, C.c_int64, C.POINTER(BinConfig), C.c_int32, _P,
@@ -136,7 +139,8 @@ EXPORTED = [
     "spgemm_pipeline_numeric_binning", "spgemm_pipeline_finalize_rpt", "spgemm_pipeline_run_numeric",
     "spgemm_pipeline_finish", "spgemm_pipeline_run", "spgemm_pipeline_rpt_region", "spgemm_pipeline_binning",
     "spgemm_pipeline_plan", "spgemm_pipeline_take_result", "spgemm_multiply", "spgemm_matrix_shape",
-    "spgemm_matrix_device_ptrs", "spgemm_matrix_download", "spgemm_matrix_free", "spgemm_compute_nprod",
+    "spgemm_matrix_device_ptrs", "spgemm_matrix_download", "spgemm_matrix_free", "spgemm_matrix_checksum",
+    "spgemm_matrix_download_async", "spgemm_ctx_wait_downloads", "spgemm_compute_nprod",
     "spgemm_build_rpt", "spgemm_run_binning",
 ]
 

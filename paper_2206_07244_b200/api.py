@@ -111,6 +111,10 @@ class Context:
     def stream(self) -> int:
         return _c.lib.spgemm_ctx_stream(self.handle) or 0
 
+    def wait_downloads(self):
+        """Wait for every DeviceMatrix.download_async issued on this context."""
+        _check(_c.lib.spgemm_ctx_wait_downloads(self.handle))
+
     def synchronize(self):
         _check(_c.lib.spgemm_ctx_synchronize(self.handle))
 
@@ -558,6 +562,24 @@ class DeviceMatrix:
         _check(_c.lib.spgemm_matrix_download(self.ctx.handle, self.handle, rpt.ctypes.data,
                                              col.ctypes.data if self.nnz else None,
                                              val.ctypes.data if self.nnz else None))
+
+    def download_async(self, rpt: np.ndarray, col: np.ndarray, val: np.ndarray, release: bool = True) -> None:
+        """Stream-ordered D2H of C on the context's copy lane (returns at once; the copy
+        overlaps whatever is queued next). Buffers (pinned for full speed) are valid after
+        Context.wait_downloads(). release=True frees C's device buffers behind the copy."""
+        if rpt.size < self.rows + 1 or col.size < self.nnz or val.size < self.nnz:
+            raise InvalidArgument("download_async: buffers too small")
+        _check(_c.lib.spgemm_matrix_download_async(self.ctx.handle, self.handle, rpt.ctypes.data,
+                                                   col.ctypes.data if self.nnz else None,
+                                                   val.ctypes.data if self.nnz else None, int(bool(release))))
+
+    def checksum(self, row_offset: int = 0, col_offset: int = 0):
+        """(sum of values, sum of (col+col_offset+1)*(row+row_offset+1) mod 2^64) on the device."""
+        v = C.c_double()
+        h = C.c_uint64()
+        _check(_c.lib.spgemm_matrix_checksum(self.ctx.handle, self.handle, int(row_offset), int(col_offset),
+                                             C.byref(v), C.byref(h)))
+        return v.value, h.value
 
     def download(self) -> CsrMatrix:
         rpt = np.empty(self.rows + 1, np.int64)

@@ -157,6 +157,8 @@ BinUpper to_upper(const spgemm_bin_config& c) {
 }
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+constexpr int kSpecCap = 128;                          // entries per row of the speculative scratch
+constexpr int64_t kSpecBudget = int64_t(4) << 30;      // scratch bytes the arena may spend on it
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
@@ -324,6 +326,7 @@ struct spgemm_pipeline {
   size_t arena_bytes = 0;
   int64_t* d_bins = nullptr;
   int64_t* d_spill = nullptr;
+  Spec spec{nullptr, nullptr, nullptr, 0};  // speculative numeric scratch (arena)
   int32_t* d_blk = nullptr;
   int* d_flags = nullptr;
   long long* d_sums = nullptr;
@@ -434,6 +437,13 @@ void spgemm_pipeline::setup() {
   off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
   const size_t o_spill = off;
   off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
+  // speculative numeric scratch (Spec in kernels.cuh): rows of the warp-group
+  // symbolic bins are multiplied during the symbolic phase
+  const bool use_spec = idx32 && M > 0 && M * kSpecCap * 12 <= kSpecBudget &&
+                        std::getenv("SPGEMM_NO_SPEC") == nullptr;
+  const size_t o_sflag = off, o_scol = align_up(o_sflag + (use_spec ? static_cast<size_t>(M) : 0), 256);
+  const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
+  if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
   arena_bytes = off;
   d_arena = static_cast<unsigned char*>(dev_alloc(arena_bytes, s));
   metadata_calls += 1;
@@ -446,6 +456,13 @@ void spgemm_pipeline::setup() {
   d_bins = reinterpret_cast<int64_t*>(d_arena + o_bins);
   d_spill = reinterpret_cast<int64_t*>(d_arena + o_spill);
   ck(cudaMemsetAsync(d_info_sym, 0, 2 * sizeof(DevInfo), s), "memset info");
+  if (use_spec) {
+    spec = Spec{reinterpret_cast<int32_t*>(d_arena + o_scol), reinterpret_cast<double*>(d_arena + o_sval),
+                d_arena + o_sflag, kSpecCap};
+    ck(cudaMemsetAsync(spec.flag, 0, static_cast<size_t>(M), s), "memset spec flags");
+  } else {
+    spec = Spec{nullptr, nullptr, nullptr, 0};
+  }
   if (M > 0) {
     SPG_LAUNCH(ctx, "k_setup_nprod", s,
                k_setup_nprod<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(A, B.rpt, d_rpt, M, sym_up,
@@ -492,17 +509,36 @@ void spgemm_pipeline::symbolic_binning() {
 // the mean B row length so the lanes striding a B row stay busy.
 // Group kernels index B with 32-bit offsets when nnz(A), nnz(B) < 2^31.
 #define SYMG(G, T, N, WB) (idx32 ? &k_sym_group<G, T, N, int32_t, WB> : &k_sym_group<G, T, N, int64_t, WB>)
-#define NUMG(G, T, E, N) (idx32 ? &k_num_group<G, T, E, N, int32_t> : &k_num_group<G, T, E, N, int64_t>)
+#define NUMG(G, T, E, N) \
+  (idx32 ? &k_num_group<G, T, E, N, int32_t, false> : &k_num_group<G, T, E, N, int64_t, false>)
 
 void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s) {
   const int64_t u = sym_plan.config.upper[bin];
   const bool g8 = avg_b_len <= 8.0;
   auto group = [&](auto kern, int G, int T, int NGRP, int WB) {
+    // Only where the numeric phase would also run a 32-lane group on a table
+    // of 256 (rows with 513..1024 products, or 257..512 when B's rows average
+    // >= 16 entries) and A's rows are
+    // regular (3-D stencils, FEM: the distinct count of such rows fits the
+    // 128-entry scratch); shorter rows are cheaper through the small kernels,
+    // and skewed rows (graphs) rarely fit.
+    const bool regular_a = M > 0 && static_cast<double>(h_sym.a_max_row) <=
+                                        4.0 * static_cast<double>(a_nnz) / static_cast<double>(M);
+    if (spec.flag != nullptr && G == 32 && u <= 1024 && regular_a && (u > 512 || (u > 256 && avg_b_len >= 16.0))) {
+      // speculative numeric first; the symbolic kernel then skips the rows it finished
+      auto sk = &k_num_group<32, 256, 4, 8, int32_t, true>;
+      const int SG = 8;
+      const size_t ssm = static_cast<size_t>(SG) * ((256 + 2) * 8 + kSpecCap * 8 + 256 * 4 + G * 16 + 16);
+      prepare_kernel(ctx, sk, ssm);
+      const int sgrid = persistent_grid(ctx, sk, G * SG, ssm, ceil_div(rl.count, SG));
+      SPG_LAUNCH(ctx, "k_num_spec<" + std::to_string(G) + ">", s,
+                 sk<<<sgrid, G * SG, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym, spec));
+    }
     const size_t smem = static_cast<size_t>(NGRP) * (static_cast<size_t>(std::max(T, WB)) * 4 + G * 16);
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
     SPG_LAUNCH(ctx, "k_sym_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
-               kern<<<grid, G * NGRP, smem, s>>>(rl, A, B, d_rpt, scale));
+               kern<<<grid, G * NGRP, smem, s>>>(rl, A, B, d_rpt, scale, spec));
   };
   auto block = [&](auto kern, int T, int threads) {
     const size_t smem = static_cast<size_t>(T) * 4;
@@ -677,11 +713,11 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
   const int64_t u = num_plan.config.upper[bin];
   const bool g8 = avg_b_len <= 8.0;
   auto group = [&](auto kern, int G, int T, int E, int NGRP) {
-    const size_t smem = static_cast<size_t>(NGRP) * ((T + 2) * 8 + G * E * 8 + T * 4 + G * 16);
+    const size_t smem = static_cast<size_t>(NGRP) * ((T + 2) * 8 + G * E * 8 + T * 4 + G * 16 + 16);
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, G * NGRP, smem, ceil_div(rl.count, NGRP));
     SPG_LAUNCH(ctx, "k_num_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
-               kern<<<grid, G * NGRP, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
+               kern<<<grid, G * NGRP, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec));
   };
   auto block = [&](auto kern, int T, int threads, int nmax) {
     const size_t smem = static_cast<size_t>(T) * 12 + static_cast<size_t>(nmax) * 8;
@@ -705,7 +741,7 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, 128, smem, ceil_div(rl.count, 128));
     SPG_LAUNCH(ctx, "k_num_thread<32,16>", s,
-               kern<<<grid, 128, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
+               kern<<<grid, 128, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec));
   } else if (u <= 32) {
     if (g8) group(NUMG(8, 64, 4, 32), 8, 64, 4, 32);
     else group(NUMG(32, 64, 1, 8), 32, 64, 1, 8);
@@ -748,6 +784,11 @@ void spgemm_pipeline::run_numeric() {
     gkeys = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(gslots) * 4 * gblocks, ctx->main_s));
     gvals = static_cast<double*>(dev_alloc(static_cast<size_t>(gslots) * 8 * gblocks, ctx->main_s));
     gbits = static_cast<uint32_t*>(dev_alloc(static_cast<size_t>(gwords) * 8 * gblocks, ctx->main_s));
+  }
+  if (spec.flag != nullptr && M > 0) {
+    const int grid = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(M, 256)));
+    SPG_LAUNCH(ctx, "k_spec_copy", ctx->main_s,
+               k_spec_copy<<<std::max(grid, 1), 256, 0, ctx->main_s>>>(spec, d_rpt, M, d_ccol, d_cval));
   }
   ck(cudaEventRecord(ctx->ev_fork, ctx->main_s), "ev_fork");
   for (int r = 0; r < kNumBins; ++r) {
@@ -1199,6 +1240,70 @@ spgemm_status spgemm_matrix_download(spgemm_ctx* ctx, const spgemm_matrix* m, in
          "D2H C.val");
     }
     ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  });
+}
+
+spgemm_status spgemm_matrix_download_async(spgemm_ctx* ctx, spgemm_matrix* m, int64_t* rpt, int32_t* col,
+                                           double* val, int32_t release) {
+  return guard([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t cs = ctx->side_s;  // the copy lane
+    cudaEvent_t ready = pooled_event(ctx);
+    ck(cudaEventRecord(ready, ctx->main_s), "record product");
+    ck(cudaStreamWaitEvent(cs, ready, 0), "copy lane waits");
+    ck(cudaMemcpyAsync(rpt, m->rpt, static_cast<size_t>(m->rows + 1) * 8, cudaMemcpyDeviceToHost, cs),
+       "D2H C.rpt");
+    if (m->nnz > 0) {
+      ck(cudaMemcpyAsync(col, m->col, static_cast<size_t>(m->nnz) * 4, cudaMemcpyDeviceToHost, cs), "D2H C.col");
+      ck(cudaMemcpyAsync(val, m->val, static_cast<size_t>(m->nnz) * 8, cudaMemcpyDeviceToHost, cs), "D2H C.val");
+    }
+    if (release) {
+      dev_free(m->rpt, cs);
+      dev_free(m->col, cs);
+      dev_free(m->val, cs);
+      m->rpt = nullptr;
+      m->col = nullptr;
+      m->val = nullptr;
+    } else {
+      // C stays owned by the handle: order the context's later work (a free
+      // of C included) behind the copy
+      cudaEvent_t done = pooled_event(ctx);
+      ck(cudaEventRecord(done, cs), "record copy");
+      ck(cudaStreamWaitEvent(ctx->main_s, done, 0), "main waits for copy");
+      ctx->ev_pool.push_back(done);
+    }
+    ctx->ev_pool.push_back(ready);  // a wait captures the record it follows, so reuse is safe
+  });
+}
+
+spgemm_status spgemm_ctx_wait_downloads(spgemm_ctx* ctx) {
+  return guard([&] {
+    DeviceGuard g(ctx->device);
+    ck(cudaStreamSynchronize(ctx->side_s), "cudaStreamSynchronize(copy lane)");
+  });
+}
+
+spgemm_status spgemm_matrix_checksum(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t row_offset,
+                                     int64_t col_offset, double* val_sum, uint64_t* pattern_hash) {
+  return guard([&] {
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = ctx->main_s;
+    void* acc = dev_alloc(16, s);
+    ck(cudaMemsetAsync(acc, 0, 16, s), "memset checksum");
+    double* dv = static_cast<double*>(acc);
+    unsigned long long* dh = reinterpret_cast<unsigned long long*>(dv + 1);
+    if (m->rows > 0) {
+      const int grid = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(m->rows, 8)));
+      SPG_LAUNCH(ctx, "k_checksum", s,
+                 k_checksum<<<std::max(grid, 1), 256, 0, s>>>(m->rpt, m->col, m->val, m->rows, row_offset,
+                                                              col_offset, dv, dh));
+    }
+    double hv[2];
+    ck(cudaMemcpyAsync(hv, acc, 16, cudaMemcpyDeviceToHost, s), "D2H checksum");
+    dev_free(acc, s);
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    *val_sum = hv[0];
+    std::memcpy(pattern_hash, &hv[1], 8);
   });
 }
 

@@ -96,6 +96,29 @@ __device__ __forceinline__ RowList RowList::resolved() const {
 }
 
 
+// Speculative numeric during the symbolic phase. Rows of the warp-group
+// symbolic bins are multiplied outright (ordered, exactly as the numeric
+// kernels do) into a scratch of `cap` entries per row; the row's count goes to
+// rpt like the symbolic kernel's and `flag` marks it done, so the symbolic
+// kernel skips it and the numeric phase only copies it into C. A row with more
+// than `cap` distinct columns is abandoned (flag stays 0) and counted by the
+// symbolic kernel as usual. The symbolic walk (~1/3 of the stencil step) is
+// saved for every row that fits.
+struct Spec {
+  int32_t* col;   // [rows * cap]
+  double* val;    // [rows * cap]
+  uint8_t* flag;  // [rows], zeroed before the symbolic phase
+  int cap;
+  __device__ __forceinline__ bool done(int64_t row) const { return flag != nullptr && flag[row] != 0; }
+};
+
+// Claim accounting of a speculative row (shared memory, one per group).
+struct ClaimBudget {
+  int* count;     // claims so far
+  int* overflow;  // set when a claim was refused
+  int cap;
+};
+
 __device__ __forceinline__ int classify_bin(long long v, const BinUpper& up) {
   int j = 0;
 #pragma unroll
@@ -188,12 +211,23 @@ __device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, const Hash& hs
 }
 
 __device__ __forceinline__ uint32_t num_slot_slow(int32_t* keys, int32_t key, const Hash& hs, uint32_t h,
-                                               int32_t cur) {
+                                               int32_t cur, const ClaimBudget* bud = nullptr,
+                                               uint32_t dummy = 0) {
   while (true) {
     if (cur == key) return h;
     if (cur == -1) {
+      if (bud) {  // speculative row: refuse claims past the budget (the row is abandoned)
+        if (*reinterpret_cast<volatile int*>(bud->count) >= bud->cap) {
+          *reinterpret_cast<volatile int*>(bud->overflow) = 1;
+          return dummy;
+        }
+      }
       cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, key);
-      if (cur == -1 || cur == key) return h;
+      if (cur == -1) {
+        if (bud) atomicAdd(bud->count, 1);
+        return h;
+      }
+      if (cur == key) return h;
     }
     h = (h + 1) & hs.mask;
     cur = *reinterpret_cast<volatile int32_t*>(keys + h);
@@ -228,7 +262,8 @@ __device__ __forceinline__ int sym_insert_batch(int32_t* tab, const int32_t (&ke
 // Slot of each key (claimed if new); invalid entries (key < 0) get `dummy`.
 template <int V>
 __device__ __forceinline__ void num_slot_batch(int32_t* keys, const int32_t (&key)[V], const Hash& hs,
-                                               uint32_t dummy, uint32_t (&slot)[V]) {
+                                               uint32_t dummy, uint32_t (&slot)[V],
+                                               const ClaimBudget* bud = nullptr) {
   int32_t cur[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) slot[v] = hs.home(key[v]) & hs.mask;
@@ -237,7 +272,7 @@ __device__ __forceinline__ void num_slot_batch(int32_t* keys, const int32_t (&ke
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     if (key[v] < 0) slot[v] = dummy;
-    else if (cur[v] != key[v]) slot[v] = num_slot_slow(keys, key[v], hs, slot[v], cur[v]);
+    else if (cur[v] != key[v]) slot[v] = num_slot_slow(keys, key[v], hs, slot[v], cur[v], bud, dummy);
   }
 }
 
@@ -685,7 +720,7 @@ template <int G, int U>
 __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
                                              int lane, unsigned gm, EntryMeta* meta, int32_t* keys,
                                              double* vals, const Hash& hs, uint32_t dummy, int32_t* kmin_out,
-                                             int32_t* kmax_out) {
+                                             int32_t* kmax_out, const ClaimBudget* bud = nullptr) {
   // The row's column range, from the first/last column of each (sorted) B row:
   // two extra loads per A entry instead of a min/max pass over the table.
   int32_t kmin = 0x7fffffff, kmax = -1;
@@ -718,7 +753,7 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
           kc[u] = ok ? B.col[at] : -1;
           x[u] = ok ? __dmul_rn(m.av, B.val[at]) : 0.0;
         }
-        num_slot_batch<U>(keys, kc, hs, dummy, slot);
+        num_slot_batch<U>(keys, kc, hs, dummy, slot, bud);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (j0 + u < nc) {
@@ -735,7 +770,7 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
           int32_t kc[1] = {q < m.len ? B.col[m.b0 + q] : -1};
           const double xv = q < m.len ? __dmul_rn(m.av, B.val[m.b0 + q]) : 0.0;
           uint32_t slot[1];
-          num_slot_batch<1>(keys, kc, hs, dummy, slot);
+          num_slot_batch<1>(keys, kc, hs, dummy, slot, bud);
           vals[slot[0]] = __dadd_rn(vals[slot[0]], xv);
         }
         __syncwarp(gm);
@@ -889,7 +924,7 @@ __device__ __forceinline__ int ceil_log2_ll(long long x) {  // x >= 1
 // (2*nprod slots, capped at T > the bin's nprod bound, so it never fills).
 template <int G, int T, int NGRP, typename IT, int WB>
 __global__ void __launch_bounds__(G* NGRP)
-    k_sym_group(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale) {
+    k_sym_group(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale, Spec sp) {
   const RowList rl = rl_in.resolved();
   static_assert(WB >= T, "bitmap region doubles as the hash table");
   constexpr int LOG_T = log2_const<T>();
@@ -902,6 +937,7 @@ __global__ void __launch_bounds__(G* NGRP)
   const Sweep sw(NGRP, threadIdx.x / G);
   for (int64_t idx = sw.first; idx < rl.count; idx += sw.next(idx)) {
     const int64_t row = rl.row(idx);
+    if (sp.done(row)) continue;  // counted by the speculative numeric kernel
     const long long np = rpt[row];
     if (np == 0) continue;  // no products: nnz 0 (pipeline.cpp:368-371)
     const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
@@ -998,7 +1034,8 @@ __global__ void __launch_bounds__(256)
 template <int TS, int NMAX>
 __global__ void __launch_bounds__(128)
     k_num_thread(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
-                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale, DevInfo* info) {
+                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale, DevInfo* info,
+                 Spec sp) {
   const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1012,6 +1049,7 @@ __global__ void __launch_bounds__(128)
     const int64_t base = rpt[row];
     const int n = static_cast<int>(rpt[row + 1] - base);
     if (n == 0) continue;
+    if (sp.done(row)) continue;  // computed in the symbolic phase, copied by k_spec_copy
 #pragma unroll
     for (int s = 0; s < TS; ++s) {
       keys[s * 32] = -1;
@@ -1252,43 +1290,62 @@ __device__ __forceinline__ void group_sort_inplace(K* buf, int n, int lane, unsi
 // row's column span allows (64 bits otherwise).
 // The 32x256 instance (3-D stencil rows) is latency-bound: capping it at 51
 // registers (5 resident blocks, 40 warps/SM) measured 3% faster than 64.
-template <int G, int T, int E, int NGRP, typename IT>
+// SPEC = the speculative numeric of the symbolic phase (see Spec): rows come
+// from a symbolic bin, the table is T slots, at most sp.cap = NMAX claims, and
+// the result goes to the Spec scratch with its count in rpt. Otherwise rows
+// already done speculatively are copied from the scratch into C.
+template <int G, int T, int E, int NGRP, typename IT, bool SPEC>
 __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
-    k_num_group(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
+    k_num_group(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt,
                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
-                DevInfo* info) {
+                DevInfo* info, Spec sp) {
   const RowList rl = rl_in.resolved();
   constexpr int NMAX = G * E;
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
-  // per group: vals[T + 2] (slot T is the dummy), packed[NMAX], keys[T], meta[G]
-  constexpr size_t kGroupBytes = (T + 2) * 8 + NMAX * 8 + T * 4 + G * 16;
+  // per group: vals[T + 2] (slot T is the dummy), packed[NMAX], keys[T], meta[G], budget
+  constexpr size_t kGroupBytes = (T + 2) * 8 + NMAX * 8 + T * 4 + G * 16 + 16;
   unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * kGroupBytes;
   double* vals = reinterpret_cast<double*>(gbase);
   unsigned long long* packed = reinterpret_cast<unsigned long long*>(gbase + (T + 2) * 8);
   uint32_t* packed32 = reinterpret_cast<uint32_t*>(packed);
   int32_t* keys = reinterpret_cast<int32_t*>(gbase + (T + 2) * 8 + NMAX * 8);
   EntryMeta* meta = reinterpret_cast<EntryMeta*>(gbase + (T + 2) * 8 + NMAX * 8 + T * 4);
+  int* budget = reinterpret_cast<int*>(gbase + (T + 2) * 8 + NMAX * 8 + T * 4 + G * 16);
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const unsigned gshift = (threadIdx.x & 31u) & ~(G - 1u);
   const Sweep sw(NGRP, grp);
   for (int64_t idx = sw.first; idx < rl.count; idx += sw.next(idx)) {
     const int64_t row = rl.row(idx);
-    const int64_t base = rpt[row];
-    const int n = static_cast<int>(rpt[row + 1] - base);
-    if (n == 0) continue;
-    const int lg = min(LOG_T, ceil_log2_ll(2 * static_cast<long long>(n)));
+    int64_t base = 0;
+    int n = 0;
+    int lg = LOG_T;
+    if constexpr (SPEC) {
+      const long long np = rpt[row];
+      if (np == 0) continue;  // no products: the symbolic kernel writes the 0
+      lg = min(LOG_T, ceil_log2_ll(2 * min(np, static_cast<long long>(NMAX))));  // nnz <= min(nprod, cap)
+    } else {
+      if (sp.done(row)) continue;  // computed in the symbolic phase, copied by k_spec_copy
+      base = rpt[row];
+      n = static_cast<int>(rpt[row + 1] - base);
+      if (n == 0) continue;
+      lg = min(LOG_T, ceil_log2_ll(2 * static_cast<long long>(n)));
+    }
     const int tsz = 1 << lg;
     const Hash hs = make_hash(scale, lg);
     fill_empty<G>(keys, tsz, lane);
     fill_zero<G>(vals, tsz, lane);
+    ClaimBudget bud{budget, budget + 1, NMAX};
+    if constexpr (SPEC) {
+      if (lane == 0) budget[0] = budget[1] = 0;
+    }
     __syncwarp(gm);
     int kmin = 0x7fffffff, kmax = -1;
     if constexpr (sizeof(IT) == 4) {
       walk_row_num<G, 4>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta, keys, vals, hs,
-                         static_cast<uint32_t>(T), &kmin, &kmax);
+                         static_cast<uint32_t>(T), &kmin, &kmax, SPEC ? &bud : nullptr);
     } else {
       walk_row<G, 4, true, true, IT>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
                                      [keys, vals, hs](int32_t key, double x) {
@@ -1311,6 +1368,16 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
         kmax = max(kmax, __shfl_xor_sync(gm, kmax, o, G));
       }
     }
+    if constexpr (SPEC) {
+      __syncwarp(gm);
+      const int claimed = *reinterpret_cast<volatile int*>(budget);
+      const bool over = *reinterpret_cast<volatile int*>(budget + 1) != 0 || claimed > NMAX;
+      __syncwarp(gm);
+      if (over) continue;  // abandoned (uniform): the symbolic kernel counts this row
+      n = claimed;
+    }
+    int32_t* ocol = SPEC ? sp.col + row * sp.cap : ccol + base;
+    double* oval = SPEC ? sp.val + row * sp.cap : cval + base;
     const bool narrow = static_cast<unsigned>(kmax - kmin) < ((0xffffffffu >> lg) - 1u);
     int run = 0;
     for (int s0 = 0; s0 < tsz; s0 += G) {
@@ -1336,16 +1403,22 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
       const uint32_t smask = (1u << lg) - 1u;
       for (int e = lane; e < n; e += G) {
         const uint32_t v = packed32[e];
-        ccol[base + e] = kmin + static_cast<int32_t>(v >> lg);
-        cval[base + e] = vals[v & smask];
+        ocol[e] = kmin + static_cast<int32_t>(v >> lg);
+        oval[e] = vals[v & smask];
       }
     } else {
       group_sort_inplace<G, E, unsigned long long>(packed, n, lane, gm);
       __syncwarp(gm);
       for (int e = lane; e < n; e += G) {
         const unsigned long long v = packed[e];
-        ccol[base + e] = static_cast<int32_t>(v >> 32);
-        cval[base + e] = vals[static_cast<uint32_t>(v)];
+        ocol[e] = static_cast<int32_t>(v >> 32);
+        oval[e] = vals[static_cast<uint32_t>(v)];
+      }
+    }
+    if constexpr (SPEC) {
+      if (lane == 0) {
+        rpt[row] = n;
+        sp.flag[row] = 1;
       }
     }
     __syncwarp(gm);
@@ -1544,6 +1617,69 @@ __global__ void __launch_bounds__(kGlobalThreads)
     }
     if (threadIdx.x == 0 && written != n) atomicOr(&info->error, kErrNumericCount);
     __syncthreads();
+  }
+}
+
+// Numeric phase, first launch: the rows finished speculatively in the symbolic
+// phase are copied from the scratch into C. A warp takes 32 consecutive rows:
+// flags and row pointers load coalesced, then the lanes copy row by row.
+__global__ void __launch_bounds__(256)
+    k_spec_copy(Spec sp, const int64_t* __restrict__ rpt, int64_t M, int32_t* __restrict__ ccol,
+                double* __restrict__ cval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; r0 < M;
+       r0 += warps * 32) {
+    const int64_t r = r0 + lane;
+    const bool mine = r < M && sp.flag[r] != 0;
+    const int64_t base = mine ? rpt[r] : 0;
+    const int n = mine ? static_cast<int>(rpt[r + 1] - base) : 0;
+    unsigned todo = __ballot_sync(kFull, mine && n > 0);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const int64_t b = __shfl_sync(kFull, base, l);
+      const int nn = __shfl_sync(kFull, n, l);
+      const int64_t s0 = (r0 + l) * sp.cap;
+      for (int e = lane; e < nn; e += 32) {
+        ccol[b + e] = sp.col[s0 + e];
+        cval[b + e] = sp.val[s0 + e];
+      }
+    }
+  }
+}
+
+// Checksums of a device CSR (streamed products): warp per row, sum of values
+// (fp64) and of (col + c0 + 1) * (row + r0 + 1) mod 2^64.
+__global__ void __launch_bounds__(256)
+    k_checksum(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col, const double* __restrict__ val,
+               int64_t rows, int64_t r0, int64_t c0, double* vsum, unsigned long long* hsum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  double v = 0.0;
+  unsigned long long h = 0;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+    const unsigned long long rr = static_cast<unsigned long long>(r + r0 + 1);
+    unsigned long long hc = 0;
+    const int64_t e1 = rpt[r + 1];
+    int64_t e = rpt[r] + lane;
+    for (; e + 96 < e1; e += 128) {  // four independent loads in flight per lane
+      const int32_t c0_ = col[e], c1_ = col[e + 32], c2_ = col[e + 64], c3_ = col[e + 96];
+      const double v0 = val[e], v1 = val[e + 32], v2 = val[e + 64], v3 = val[e + 96];
+      hc += static_cast<unsigned long long>(c0_) + c1_ + c2_ + c3_ + 4 * (c0 + 1);
+      v += (v0 + v1) + (v2 + v3);
+    }
+    for (; e < e1; e += 32) {
+      hc += static_cast<unsigned long long>(col[e] + c0 + 1);
+      v += val[e];
+    }
+    h += hc * rr;
+  }
+  v = warp_sum(v);
+  h = warp_sum(h);
+  if (lane == 0) {
+    atomicAdd(vsum, v);
+    atomicAdd(hsum, h);
   }
 }
 

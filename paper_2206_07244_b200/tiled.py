@@ -70,16 +70,21 @@ def split_columns(b: CsrMatrix, window: int = WINDOW) -> List[CsrMatrix]:
 
 
 def row_blocks(nprod: np.ndarray, budget: int) -> List[int]:
-    """Contiguous row blocks with at most ``budget`` products each (a single row
+    """Contiguous row blocks of at most ``budget`` products each (a single row
     above the budget forms its own block). Returns the block boundaries."""
+    nprod = np.asarray(nprod, np.int64)
+    cs = np.cumsum(nprod)
+    total = int(cs[-1]) if cs.size else 0
     bounds = [0]
-    acc = 0
-    for i, p in enumerate(np.asarray(nprod, np.int64)):
-        if acc and acc + p > budget:
-            bounds.append(i)
-            acc = 0
-        acc += int(p)
-    bounds.append(int(len(nprod)))
+    base = 0  # products before the current block
+    while bounds[-1] < nprod.size and total - base > budget:
+        # first row whose inclusive prefix exceeds base + budget ends the block
+        i = int(np.searchsorted(cs, base + budget, side="right"))
+        i = max(i, bounds[-1] + 1)  # a row above the budget: a block of its own
+        bounds.append(i)
+        base = int(cs[i - 1])
+    if bounds[-1] < nprod.size:
+        bounds.append(int(nprod.size))
     return bounds
 
 
@@ -101,36 +106,23 @@ class StreamReport:
 
 
 def _tile_checksum(dm, row0: int, col0: int):
-    torch = _torch()
-    if dm.nnz == 0:
-        return 0.0, 0
-
-    class _V:
-        def __init__(self, ptr, n, typestr):
-            self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
-
-    rpt = torch.as_tensor(_V(dm.ptrs[0], dm.rows + 1, "<i8"), device="cuda")
-    col = torch.as_tensor(_V(dm.ptrs[1], dm.nnz, "<i4"), device="cuda")
-    val = torch.as_tensor(_V(dm.ptrs[2], dm.nnz, "<f8"), device="cuda")
-    rows = torch.repeat_interleave(torch.arange(dm.rows, device=col.device, dtype=torch.int64) + (row0 + 1),
-                                   rpt[1:] - rpt[:-1])
-    h = int(((col.to(torch.int64) + (col0 + 1)) * rows).sum().item()) & ((1 << 64) - 1)
-    return float(val.sum().item()), h
+    return dm.checksum(row0, col0) if dm.nnz else (0.0, 0)
 
 
 def stream_multiply(a: CsrMatrix, b: CsrMatrix, rows: Optional[range] = None, nprod: Optional[np.ndarray] = None,
                     budget: int = 4_000_000_000, window: int = WINDOW, b_windows: Optional[List[CsrMatrix]] = None,
                     device: Optional[int] = None, options=None) -> StreamReport:
     """C = A[rows].B computed tile by tile (row blocks x column windows) and
-    streamed into checksums. ``nprod`` (per row of A, from K1) and ``b_windows``
-    can be passed in to share them across calls."""
+    streamed into checksums. A row block holds at most ``budget`` products over
+    all windows, so no tile's C exceeds 12 * budget bytes. ``nprod`` (per row of
+    A, from K1) and ``b_windows`` can be passed in to share them across calls."""
     if nprod is None:
         nprod, _ = compute_nprod(a, b, device=device)
     nprod = np.asarray(nprod, np.int64)
     r_lo, r_hi = (0, a.rows) if rows is None else (rows.start, rows.stop)
     wins = b_windows if b_windows is not None else split_columns(b, window)
     rep = StreamReport()
-    bounds = row_blocks(nprod[r_lo:r_hi], max(1, budget // max(1, len(wins))))
+    bounds = row_blocks(nprod[r_lo:r_hi], max(1, budget))
     for i in range(len(bounds) - 1):
         r0, r1 = r_lo + bounds[i], r_lo + bounds[i + 1]
         if r1 <= r0:

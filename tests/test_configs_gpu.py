@@ -83,3 +83,26 @@ def test_virtual_row_slices_stitch_bitwise(sg, oracle):
         b = nprod_split(nprod, parts)
         slices = [sg.multiply(slice_rows(a, b[g], b[g + 1]), a).c for g in range(parts)]
         assert stitch(slices, a.cols) == single
+
+
+def test_download_async_matches_sync(sg, oracle):
+    """DeviceMatrix.download_async (copy lane, device buffers released behind the copy)
+    delivers the same C as the synchronous download, also when the next product is
+    queued before the wait."""
+    import torch
+    a = S.random_values(S.stencil3d_27pt(20), 4)
+    ctx = sg.get_context()
+    exp = oracle.spgemm(a, a)
+    bufs = []
+    for _ in range(2):
+        dm, _ = sg.multiply_device(a, a)
+        r = torch.empty(a.rows + 1, dtype=torch.int64).pin_memory()
+        c = torch.empty(dm.nnz, dtype=torch.int32).pin_memory()
+        v = torch.empty(dm.nnz, dtype=torch.float64).pin_memory()
+        dm.download_async(r.numpy(), c.numpy(), v.numpy(), release=True)
+        dm.free()
+        bufs.append((r, c, v))
+    ctx.wait_downloads()
+    for r, c, v in bufs:
+        got = sg.CsrMatrix(a.rows, a.cols, r.numpy(), c.numpy(), v.numpy())
+        assert_matches_oracle(got, exp, bitwise=True)
