@@ -164,13 +164,22 @@ def run_reference(args):
         return
     from oracle import oracle as O
     from paper_2206_07244_b200.api import CsrMatrix
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    workload = CONFIG_NAMES[args.config]
     if args.config == 5:
         from paper_2206_07244_b200 import synthetic as S
         mats = [S.rmat(args.rmat_scale, 16, seed=args.rmat_scale)] * 2
+    elif world > 1 and args.config == 2:
+        # the b200 arm's N-GPU workload (weak scaling): sampled the same way
+        g = stencil_weak(world)
+        mats = [g, g]
+        workload = f"C=A*A 3D 27-pt stencil 128x128x{128 * world} (weak: 128^3 rows/GPU), nprod-balanced row blocks"
     else:
         mats = build_workload(args.config)
     a = mats[0]
     frac = {1: 1.0, 2: 0.25, 3: 0.02, 4: 1.0, 5: 0.0005}[args.config]
+    if args.config == 2 and world > 1:
+        frac /= world  # same sample size as at N=1 (the weak-scaled matrix is N x larger)
     r0 = int(a.rows * (0.5 - frac / 2)) if frac < 1 else 0
     r1 = r0 + int(a.rows * frac) if frac < 1 else a.rows
     rpt = a.rpt[r0:r1 + 1] - a.rpt[r0]
@@ -199,7 +208,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], "sample_rows": [r0, r1]},
+        "config": {"workload": workload, "sample_rows": [r0, r1]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"rows [{r0},{r1}) of config {args.config}'s A times B per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

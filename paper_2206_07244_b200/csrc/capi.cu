@@ -531,7 +531,7 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
       const size_t ssm = static_cast<size_t>(SG) * ((256 + 2) * 8 + kSpecCap * 8 + 256 * 4 + G * 16 + 16);
       prepare_kernel(ctx, sk, ssm);
       const int sgrid = persistent_grid(ctx, sk, G * SG, ssm, ceil_div(rl.count, SG));
-      SPG_LAUNCH(ctx, "k_num_spec<" + std::to_string(G) + ">", s,
+      SPG_LAUNCH(ctx, "k_num_group<" + std::to_string(G) + ",256,spec>", s,
                  sk<<<sgrid, G * SG, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym, spec));
     }
     const size_t smem = static_cast<size_t>(NGRP) * (static_cast<size_t>(std::max(T, WB)) * 4 + G * 16);
