@@ -1380,20 +1380,37 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
     double* oval = SPEC ? sp.val + row * sp.cap : cval + base;
     const bool narrow = static_cast<unsigned>(kmax - kmin) < ((0xffffffffu >> lg) - 1u);
     int run = 0;
-    for (int s0 = 0; s0 < tsz; s0 += G) {
-      const int s = s0 + lane;
-      const int32_t key = s < tsz ? keys[s] : -1;
-      const bool occ = key != -1;
-      const unsigned bal = __ballot_sync(gm, occ) >> gshift;
-      if (occ) {
-        const int at = run + __popc(bal & ((1u << lane) - 1u));
-        if (narrow)
-          packed32[at] = (static_cast<uint32_t>(key - kmin) << lg) | static_cast<uint32_t>(s);
-        else
-          packed[at] = (static_cast<unsigned long long>(static_cast<uint32_t>(key)) << 32) |
-                       static_cast<uint32_t>(s);
+    auto emit = [&](int at, int32_t key, int s) {
+      if (narrow)
+        packed32[at] = (static_cast<uint32_t>(key - kmin) << lg) | static_cast<uint32_t>(s);
+      else
+        packed[at] = (static_cast<unsigned long long>(static_cast<uint32_t>(key)) << 32) | static_cast<uint32_t>(s);
+    };
+    if (tsz >= 4 * G) {
+      // 4 slots per lane per pass (one 16-byte load); a lane's rank is the
+      // count of occupied slots in lower lanes over the 4 per-position ballots
+      const unsigned lt = (1u << lane) - 1u;
+      for (int s0 = 0; s0 < tsz; s0 += 4 * G) {
+        const int4 k4 = reinterpret_cast<const int4*>(keys + s0)[lane];
+        const unsigned b0 = __ballot_sync(gm, k4.x != -1) >> gshift, b1 = __ballot_sync(gm, k4.y != -1) >> gshift;
+        const unsigned b2 = __ballot_sync(gm, k4.z != -1) >> gshift, b3 = __ballot_sync(gm, k4.w != -1) >> gshift;
+        int at = run + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+        const int s = s0 + 4 * lane;
+        if (k4.x != -1) emit(at++, k4.x, s);
+        if (k4.y != -1) emit(at++, k4.y, s + 1);
+        if (k4.z != -1) emit(at++, k4.z, s + 2);
+        if (k4.w != -1) emit(at++, k4.w, s + 3);
+        run += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
       }
-      run += __popc(bal);
+    } else {
+      for (int s0 = 0; s0 < tsz; s0 += G) {
+        const int s = s0 + lane;
+        const int32_t key = s < tsz ? keys[s] : -1;
+        const bool occ = key != -1;
+        const unsigned bal = __ballot_sync(gm, occ) >> gshift;
+        if (occ) emit(run + __popc(bal & ((1u << lane) - 1u)), key, s);
+        run += __popc(bal);
+      }
     }
     if (run != n && lane == 0) atomicOr(&info->error, kErrNumericCount);
     __syncwarp(gm);
