@@ -327,6 +327,7 @@ struct spgemm_pipeline {
   int64_t* d_bins = nullptr;
   int64_t* d_spill = nullptr;
   Spec spec{nullptr, nullptr, nullptr, 0};  // speculative numeric scratch (arena)
+  bool regular_a = false;                    // A's longest row <= 4x its mean (set by setup)
   int32_t* d_blk = nullptr;
   int* d_flags = nullptr;
   long long* d_sums = nullptr;
@@ -420,49 +421,19 @@ void spgemm_pipeline::setup() {
   cudaStream_t s = ctx->main_s;
   nrb = ceil_div(M, kRowsPerBlock);
   ntiles = ceil_div(M + 1, kScanTile);
-  d_rpt = static_cast<int64_t*>(dev_alloc(static_cast<size_t>(M + 1) * 8, s));
-  metadata_calls += 1;
-  metadata_bytes += (M + 1) * 8;
-  // One arena for all binning metadata, sized from the row count alone.
-  size_t off = 0;
-  const size_t o_info = off;
-  off = align_up(off + 2 * sizeof(DevInfo), 256);
-  const size_t o_blk = off;
-  off = align_up(off + static_cast<size_t>(std::max<int64_t>(nrb, 1)) * kNumBins * 4, 256);
-  const size_t o_flags = off;
-  off = align_up(off + static_cast<size_t>(ntiles) * 4, 256);
-  const size_t o_sums = off;
-  off = align_up(off + static_cast<size_t>(ntiles) * 16, 256);
-  const size_t o_bins = off;  // row ids as int64, the reference's BinningResult layout
-  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
-  const size_t o_spill = off;
-  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
-  // speculative numeric scratch (Spec in kernels.cuh): rows of the warp-group
-  // symbolic bins are multiplied during the symbolic phase
-  const bool use_spec = idx32 && M > 0 && M * kSpecCap * 12 <= kSpecBudget &&
-                        std::getenv("SPGEMM_NO_SPEC") == nullptr;
-  const size_t o_sflag = off, o_scol = align_up(o_sflag + (use_spec ? static_cast<size_t>(M) : 0), 256);
-  const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
-  if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
-  arena_bytes = off;
-  d_arena = static_cast<unsigned char*>(dev_alloc(arena_bytes, s));
-  metadata_calls += 1;
-  metadata_bytes += static_cast<int64_t>(arena_bytes);
-  d_info_sym = reinterpret_cast<DevInfo*>(d_arena + o_info);
+  // Allocation 1: C.rpt, with K1's outputs behind it (phase scalars and the
+  // per-row-block bin counts), so the arena can be sized after K1.
+  const size_t o_info = align_up(static_cast<size_t>(M + 1) * 8, 256);
+  const size_t o_blk = align_up(o_info + 2 * sizeof(DevInfo), 256);
+  const size_t rpt_bytes = align_up(o_blk + static_cast<size_t>(std::max<int64_t>(nrb, 1)) * kNumBins * 4, 256);
+  unsigned char* head = static_cast<unsigned char*>(dev_alloc(rpt_bytes, s));
+  d_rpt = reinterpret_cast<int64_t*>(head);
+  d_info_sym = reinterpret_cast<DevInfo*>(head + o_info);
   d_info_num = d_info_sym + 1;
-  d_blk = reinterpret_cast<int32_t*>(d_arena + o_blk);
-  d_flags = reinterpret_cast<int*>(d_arena + o_flags);
-  d_sums = reinterpret_cast<long long*>(d_arena + o_sums);
-  d_bins = reinterpret_cast<int64_t*>(d_arena + o_bins);
-  d_spill = reinterpret_cast<int64_t*>(d_arena + o_spill);
+  d_blk = reinterpret_cast<int32_t*>(head + o_blk);
+  metadata_calls += 1;
+  metadata_bytes += static_cast<int64_t>(rpt_bytes);
   ck(cudaMemsetAsync(d_info_sym, 0, 2 * sizeof(DevInfo), s), "memset info");
-  if (use_spec) {
-    spec = Spec{reinterpret_cast<int32_t*>(d_arena + o_scol), reinterpret_cast<double*>(d_arena + o_sval),
-                d_arena + o_sflag, kSpecCap};
-    ck(cudaMemsetAsync(spec.flag, 0, static_cast<size_t>(M), s), "memset spec flags");
-  } else {
-    spec = Spec{nullptr, nullptr, nullptr, 0};
-  }
   if (M > 0) {
     SPG_LAUNCH(ctx, "k_setup_nprod", s,
                k_setup_nprod<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(A, B.rpt, d_rpt, M, sym_up,
@@ -474,6 +445,39 @@ void spgemm_pipeline::setup() {
   if (h_sym.total > static_cast<unsigned long long>(std::numeric_limits<int64_t>::max()))
     fail(SPGEMM_OVERFLOW, "spgemm: intermediate-product count overflowed 64 bits");
   total_nprod = static_cast<int64_t>(h_sym.total);
+  // Allocation 2: the arena -- scan state, bin row ids, spill ids and, when
+  // some symbolic bin will run it, the speculative-numeric scratch (Spec in
+  // kernels.cuh), decided now that K1 has reported A's row statistics.
+  size_t off = 0;
+  const size_t o_flags = off;
+  off = align_up(off + static_cast<size_t>(ntiles) * 4, 256);
+  const size_t o_sums = off;
+  off = align_up(off + static_cast<size_t>(ntiles) * 16, 256);
+  const size_t o_bins = off;  // row ids as int64, the reference's BinningResult layout
+  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
+  const size_t o_spill = off;
+  off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
+  regular_a = M > 0 && static_cast<double>(h_sym.a_max_row) <= 4.0 * static_cast<double>(a_nnz) / static_cast<double>(M);
+  const bool use_spec = idx32 && M > 0 && avg_b_len > 8.0 && regular_a && M * kSpecCap * 12 <= kSpecBudget &&
+                        std::getenv("SPGEMM_NO_SPEC") == nullptr;
+  const size_t o_sflag = off, o_scol = align_up(o_sflag + (use_spec ? static_cast<size_t>(M) : 0), 256);
+  const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
+  if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
+  arena_bytes = off;
+  d_arena = static_cast<unsigned char*>(dev_alloc(arena_bytes, s));
+  metadata_calls += 1;
+  metadata_bytes += static_cast<int64_t>(arena_bytes);
+  d_flags = reinterpret_cast<int*>(d_arena + o_flags);
+  d_sums = reinterpret_cast<long long*>(d_arena + o_sums);
+  d_bins = reinterpret_cast<int64_t*>(d_arena + o_bins);
+  d_spill = reinterpret_cast<int64_t*>(d_arena + o_spill);
+  if (use_spec) {
+    spec = Spec{reinterpret_cast<int32_t*>(d_arena + o_scol), reinterpret_cast<double*>(d_arena + o_sval),
+                d_arena + o_sflag, kSpecCap};
+    ck(cudaMemsetAsync(spec.flag, 0, static_cast<size_t>(M), s), "memset spec flags");
+  } else {
+    spec = Spec{nullptr, nullptr, nullptr, 0};
+  }
   mark(1);
   stage = kSetup;
 }
@@ -522,8 +526,6 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     // regular (3-D stencils, FEM: the distinct count of such rows fits the
     // 128-entry scratch); shorter rows are cheaper through the small kernels,
     // and skewed rows (graphs) rarely fit.
-    const bool regular_a = M > 0 && static_cast<double>(h_sym.a_max_row) <=
-                                        4.0 * static_cast<double>(a_nnz) / static_cast<double>(M);
     if (spec.flag != nullptr && G == 32 && u <= 1024 && regular_a && (u > 512 || (u > 256 && avg_b_len >= 16.0))) {
       // speculative numeric first; the symbolic kernel then skips the rows it finished
       auto sk = &k_num_group<32, 256, 4, 8, int32_t, true>;

@@ -37,12 +37,3 @@ def test_split_columns_partition(sg):
     for w in wins:
         c = w.col.cpu().numpy()
         assert c.size == 0 or (c.min() >= 0 and c.max() < w.cols)
-
-
-def test_row_blocks_budget():
-    nprod = np.array([5, 5, 5, 20, 1, 1, 1], np.int64)
-    b = T.row_blocks(nprod, 10)
-    assert b[0] == 0 and b[-1] == nprod.size
-    for i in range(len(b) - 1):
-        blk = nprod[b[i]:b[i + 1]]
-        assert blk.sum() <= 10 or blk.size == 1
