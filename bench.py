@@ -452,7 +452,7 @@ def main():
     # ----------------------------------------------------------------- e2e
     e2e = None
     if rank == 0 and host_ops is not None and args.config in (1, 2):
-        e2e = run_e2e(sg, torch, host_ops[0], max(3, args.e2e_steps or args.steps // 4), local)
+        e2e = run_e2e(sg, torch, host_ops[0], max(8, args.e2e_steps or args.steps // 2), local)
     elif rank == 0:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                "note": "e2e measured on configs 1-2 (config 3's C is 116.7 GB; config 4 chains on device)"}

@@ -1232,16 +1232,22 @@ spgemm_status spgemm_matrix_download(spgemm_ctx* ctx, const spgemm_matrix* m, in
                                      int32_t* col, double* val) {
   return guard([&] {
     DeviceGuard g(ctx->device);
-    cudaStream_t s = ctx->main_s;
-    ck(cudaMemcpyAsync(rpt, m->rpt, static_cast<size_t>(m->rows + 1) * 8, cudaMemcpyDeviceToHost, s),
+    // on the copy lane, behind the work queued on the context's stream (the
+    // product): the compute stream is not held by the transfer
+    cudaStream_t cs = ctx->side_s;
+    cudaEvent_t ready = pooled_event(ctx);
+    ck(cudaEventRecord(ready, ctx->main_s), "record product");
+    ck(cudaStreamWaitEvent(cs, ready, 0), "copy lane waits");
+    ctx->ev_pool.push_back(ready);
+    ck(cudaMemcpyAsync(rpt, m->rpt, static_cast<size_t>(m->rows + 1) * 8, cudaMemcpyDeviceToHost, cs),
        "D2H C.rpt");
     if (m->nnz > 0) {
-      ck(cudaMemcpyAsync(col, m->col, static_cast<size_t>(m->nnz) * 4, cudaMemcpyDeviceToHost, s),
+      ck(cudaMemcpyAsync(col, m->col, static_cast<size_t>(m->nnz) * 4, cudaMemcpyDeviceToHost, cs),
          "D2H C.col");
-      ck(cudaMemcpyAsync(val, m->val, static_cast<size_t>(m->nnz) * 8, cudaMemcpyDeviceToHost, s),
+      ck(cudaMemcpyAsync(val, m->val, static_cast<size_t>(m->nnz) * 8, cudaMemcpyDeviceToHost, cs),
          "D2H C.val");
     }
-    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    ck(cudaStreamSynchronize(cs), "cudaStreamSynchronize(copy lane)");
   });
 }
 
