@@ -27,7 +27,8 @@ def short_name(full):
         keep = [a for a in args if a.isdigit()]
         if name in ("k_sym_group", "k_num_group"):
             keep = keep[:2]
-            if name == "k_num_group" and "true" in targs:
+            last = targs[1:-1].split(",")[-1].strip().replace("(bool)", "")
+            if name == "k_num_group" and last in ("1", "true"):
                 keep.append("spec")  # the speculative instance of the symbolic phase
         elif name in ("k_sym_block", "k_num_block"):
             keep = keep[:1]
