@@ -213,6 +213,29 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   }
 }
 
+// C.val of the rows in flight is zeroed and then hit by atomic adds from the
+// whole row; both go out with an evict-last L2 policy so the lines stay
+// on chip between the two while the B gathers stream through L2.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+#ifdef SPGEMM_ABLATE_NOKEEP
+  *p = v;
+#else
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#endif
+}
+__device__ __forceinline__ void red_add_keep(double* p, double v, uint64_t pol) {
+#ifdef SPGEMM_ABLATE_NOKEEP
+  atomicAdd(p, v);
+#else
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#endif
+}
+
 // Numeric heap tier (see the header comment).
 __global__ void __launch_bounds__(kBigThreads, 1)
     k_big_num(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
@@ -226,6 +249,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   BigTile& t = *reinterpret_cast<BigTile*>(smem_raw + sizeof(uint32_t) * kBigWordsPad +
                                            sizeof(uint16_t) * kBigPrePad + sizeof(uint32_t) * (kBigWords / kBigSuper));
   const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t keep = l2_evict_last_policy();
   for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
     const int64_t row = rl.row(idx);
     const int64_t base = rpt[row];
@@ -276,7 +300,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
           } while (m);
         }
       }
-      for (int64_t e = tid; e < wtot; e += kBigThreads) cval[base + woff + e] = 0.0;
+      for (int64_t e = tid; e < wtot; e += kBigThreads) st_keep(cval + base + woff + e, 0.0, keep);
       __syncthreads();  // rank directory + zeroed C.val visible to the block
       // ---- pass B: products accumulate at their rank
       double* crow = cval + base + woff;
@@ -287,7 +311,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
           const uint32_t w = off >> 5;
           const uint32_t r = sup[w / kBigSuper] + pre[pre_idx(w)] + __popc(bm[bm_idx(w)] & ((1u << (off & 31u)) - 1u));
 #ifndef SPGEMM_ABLATE_RED
-          atomicAdd(crow + r, x);
+          red_add_keep(crow + r, x, keep);
 #else
           if (x == 1.2345e-300) crow[r] = x;
 #endif
