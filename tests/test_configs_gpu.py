@@ -106,3 +106,30 @@ def test_download_async_matches_sync(sg, oracle):
     for r, c, v in bufs:
         got = sg.CsrMatrix(a.rows, a.cols, r.numpy(), c.numpy(), v.numpy())
         assert_matches_oracle(got, exp, bitwise=True)
+
+
+def test_speculative_rows_mixed_with_abandoned(sg, oracle):
+    """Regular A (28 entries per row, long B rows) puts every row in a symbolic bin the
+    speculative numeric runs on: stencil rows fit its 128-entry scratch and are finished
+    there, scattered random rows (~700 distinct columns) overflow it, are abandoned and
+    go through the symbolic + numeric kernels. Both kinds in one product, bitwise."""
+    from helpers import random_csr_fixed
+    from paper_2206_07244_b200.distributed import slice_rows
+    sten = S.random_values(S.stencil3d_27pt(14), 2)            # 27 entries/row, CR ~6
+    rnd = random_csr_fixed(sten.rows, sten.cols, 28, 8)         # 28 entries/row, CR ~1
+    rnd = S.random_values(rnd, 3)
+    # interleave: rows alternate between the stencil and the random matrix
+    rows = sten.rows
+    pick = np.arange(rows) % 2 == 0
+    import numpy as _np
+    rpt = _np.zeros(rows + 1, _np.int64)
+    lens = _np.where(pick, _np.diff(sten.rpt), _np.diff(rnd.rpt))
+    _np.cumsum(lens, out=rpt[1:])
+    col = _np.concatenate([(sten if pick[i] else rnd).row_cols(i) for i in range(rows)])
+    val = _np.concatenate([(sten if pick[i] else rnd).row_vals(i) for i in range(rows)])
+    a = sg.CsrMatrix(rows, sten.cols, rpt, col.astype(_np.int32), val)
+    out = sg.multiply(a, a)
+    exp = oracle.spgemm(a, a)
+    assert_matches_oracle(out.c, exp, bitwise=True)
+    nnz = np.diff(exp.rpt)
+    assert (nnz[pick] <= 128).any() and (nnz[~pick] > 128).any()
