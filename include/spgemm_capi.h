@@ -211,6 +211,21 @@ spgemm_status spgemm_ctx_wait_downloads(spgemm_ctx* ctx);
 spgemm_status spgemm_matrix_checksum(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t row_offset,
                                      int64_t col_offset, double* val_sum, uint64_t* pattern_hash);
 
+/* ------------------------------------------------ several GPUs, one process */
+/* B200 extension (§8(b)'s spgemm_multiply_multi): C = A*B over
+ * n contexts (normally one per device). A's rows are split into contiguous
+ * blocks balanced by the prefix sum of per-row products (row_bounds[0..n]);
+ * every context multiplies its block by all of B on its own host thread and
+ * keeps its slice of C on its device (slices[0..n)). Host-resident operands
+ * when n > 1. report: summed counts, the slowest block's timings. */
+spgemm_status spgemm_multiply_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_csr_view* a,
+                                    const spgemm_csr_view* b, const spgemm_options* opts,
+                                    spgemm_matrix** slices, int64_t* row_bounds, spgemm_report* report);
+/* Downloads the slices of spgemm_multiply_multi into one host CSR (rows+1,
+ * nnz, nnz entries), row pointers stitched with the slices' nnz offsets. */
+spgemm_status spgemm_matrices_download_stitched(spgemm_ctx** ctxs, spgemm_matrix* const* slices, int32_t n,
+                                                int64_t* rpt, int32_t* col, double* val);
+
 /* ----------------------------------------------- standalone GPU kernels */
 /* compute_nprod() (reference.cpp:37-55) on the device: out[M] host or device. */
 spgemm_status spgemm_compute_nprod(spgemm_ctx* ctx, const spgemm_csr_view* a,

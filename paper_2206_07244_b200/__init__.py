@@ -9,5 +9,5 @@ from .api import (  # noqa: F401
     SpgemmPipeline, StepTimings, SYMBOLIC, NUMERIC, build_rpt, classify, compute_nprod, get_context,
     kDefaultNumPreset, kDefaultSymPreset, kMaxSymbolicTableSize, kNoUpperBound, kNumBins,
     kSymbolicSpillThreshold, make_execution_plan, max_relative_error, multiply, multiply_device,
-    numeric_preset, preset, preset_names, run_binning, same_pattern, symbolic_preset, validate_csr,
+    multiply_multi, numeric_preset, preset, preset_names, run_binning, same_pattern, symbolic_preset, validate_csr,
 )

@@ -125,6 +125,8 @@ _decl("spgemm_matrix_free", None, [_P])
 _decl("spgemm_matrix_checksum", _st, [_P, _P, C.c_int64, C.c_int64, _P, _P])
 _decl("spgemm_matrix_download_async", _st, [_P, _P, _P, _P, _P, C.c_int32])
 _decl("spgemm_ctx_wait_downloads", _st, [_P])
+_decl("spgemm_multiply_multi", _st, [_P, C.c_int32, _P, _P, _P, _P, _P, _P])
+_decl("spgemm_matrices_download_stitched", _st, [_P, _P, C.c_int32, _P, _P, _P])
 _decl("spgemm_compute_nprod", _st, [_P, C.POINTER(CsrView), C.POINTER(CsrView), _P, C.POINTER(C.c_int64)])
 _decl("spgemm_build_rpt", _st, [_P, _P, C.c_int64, C.POINTER(C.c_int64)])
 _decl("spgemm_run_binning", _st, [_P, _P, C.c_int64, C.POINTER(BinConfig), C.c_int32, _P,
@@ -140,7 +142,8 @@ EXPORTED = [
     "spgemm_pipeline_finish", "spgemm_pipeline_run", "spgemm_pipeline_rpt_region", "spgemm_pipeline_binning",
     "spgemm_pipeline_plan", "spgemm_pipeline_take_result", "spgemm_multiply", "spgemm_matrix_shape",
     "spgemm_matrix_device_ptrs", "spgemm_matrix_download", "spgemm_matrix_free", "spgemm_matrix_checksum",
-    "spgemm_matrix_download_async", "spgemm_ctx_wait_downloads", "spgemm_compute_nprod",
+    "spgemm_matrix_download_async", "spgemm_ctx_wait_downloads", "spgemm_multiply_multi",
+    "spgemm_matrices_download_stitched", "spgemm_compute_nprod",
     "spgemm_build_rpt", "spgemm_run_binning",
 ]
 

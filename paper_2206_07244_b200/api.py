@@ -715,6 +715,47 @@ def multiply(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] = None
         p.close()
 
 
+def multiply_multi(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] = None,
+                   devices: Sequence[int] = (0,)) -> SpgemmOutput:
+    """SURVEY.md §8(e) inside one process (C ABI spgemm_multiply_multi): A's rows split
+    by the nprod prefix sum over `devices` (an index may repeat: one fresh context per
+    entry), every block multiplied by all of B on its own host thread, C stitched on the
+    host. `row_bounds` of the split is attached to the returned SpgemmOutput."""
+    devices = list(devices)
+    if not devices:
+        raise InvalidArgument("multiply_multi: no devices")
+    ctxs = [Context(d) for d in devices]
+    n = len(ctxs)
+    handles = (C.c_void_p * n)(*[c.handle for c in ctxs])
+    slices = (C.c_void_p * n)()
+    bounds = (C.c_int64 * (n + 1))()
+    rep = _c.Report()
+    va, vb = a._view(), b._view()
+    opts = options._c() if options is not None else None
+    try:
+        _check(_c.lib.spgemm_multiply_multi(handles, n, C.byref(va), C.byref(vb),
+                                            C.byref(opts) if opts is not None else None, slices, bounds,
+                                            C.byref(rep)))
+        nnz = int(rep.nnz_of_product)
+        rpt = np.empty(a.rows + 1, np.int64)
+        col = np.empty(nnz, np.int32)
+        val = np.empty(nnz, np.float64)
+        try:
+            _check(_c.lib.spgemm_matrices_download_stitched(handles, slices, n, rpt.ctypes.data,
+                                                            col.ctypes.data if nnz else None,
+                                                            val.ctypes.data if nnz else None))
+        finally:
+            for h in slices:
+                if h:
+                    _c.lib.spgemm_matrix_free(h)
+    finally:
+        for c in ctxs:
+            c.close()
+    out = _output_from(rep, CsrMatrix(a.rows, b.cols, rpt, col, val), options)
+    out.row_bounds = [int(x) for x in bounds]
+    return out
+
+
 def multiply_device(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] = None,
                     device: Optional[int] = None):
     """C = A*B with C left in HBM. Returns (DeviceMatrix, SpgemmOutput with c=None)."""

@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libspgemm_b200.so")
 SOURCES = [os.path.join(CSRC, "capi.cu")]
-CXX_SOURCES = [os.path.join(CSRC, "cxx_api.cpp")]  # the reference's C++ API over the C ABI
+CXX_SOURCES = [os.path.join(CSRC, "cxx_api.cpp"), os.path.join(CSRC, "multi.cpp")]  # the reference's C++ API over the C ABI
 HEADERS = [os.path.join(ROOT, "include", "spgemm_capi.h")] + [
     os.path.join(ROOT, "include", "spgemm", h) for h in sorted(os.listdir(os.path.join(ROOT, "include", "spgemm")))]
 DEPS = SOURCES + CXX_SOURCES + HEADERS + [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "kernels_heap.cuh")]

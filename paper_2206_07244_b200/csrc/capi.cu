@@ -881,6 +881,10 @@ extern "C" {
 
 const char* spgemm_last_error(void) { return g_err.c_str(); }
 
+// not in the public header: lets multi.cpp report a worker thread's error on
+// the calling thread
+void spgemm_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
+
 void spgemm_options_default(spgemm_options* o) {
   std::memset(o, 0, sizeof(*o));
   std::strncpy(o->sym_preset, "sym_1.2x", sizeof(o->sym_preset) - 1);

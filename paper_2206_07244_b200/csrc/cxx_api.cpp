@@ -67,6 +67,28 @@ spgemm_csr_view view(const CsrMatrix& m) {
   return spgemm_csr_view{m.rows, m.cols, m.rpt.data(), m.col.data(), m.val.data(), 0};
 }
 
+spgemm_options to_c_options(const SpgemmOptions& options) {
+  spgemm_options o;
+  spgemm_options_default(&o);
+  std::snprintf(o.sym_preset, sizeof(o.sym_preset), "%s", options.sym_preset.c_str());
+  std::snprintf(o.num_preset, sizeof(o.num_preset), "%s", options.num_preset.c_str());
+  o.workers = options.workers;
+  o.overlap = options.overlap ? 1 : 0;
+  o.deterministic = options.deterministic ? 1 : 0;
+  o.chunk_rows = options.chunk_rows;
+  o.hash_scale = options.hash.hash_scale;
+  o.ordered_heap = options.ordered_heap ? 1 : 0;
+  if (options.sym_launch_order) {
+    o.has_sym_launch_order = 1;
+    std::copy(options.sym_launch_order->begin(), options.sym_launch_order->end(), o.sym_launch_order);
+  }
+  if (options.num_launch_order) {
+    o.has_num_launch_order = 1;
+    std::copy(options.num_launch_order->begin(), options.num_launch_order->end(), o.num_launch_order);
+  }
+  return o;
+}
+
 spgemm_bin_config to_c(const BinConfig& c) {
   spgemm_bin_config out;
   std::memset(&out, 0, sizeof(out));
@@ -357,24 +379,7 @@ SpgemmPipeline::SpgemmPipeline(const CsrMatrix& a, const CsrMatrix& b, const Spg
       options_(options),
       sym_plan_(make_execution_plan(symbolic_preset(options.sym_preset))),
       num_plan_(make_execution_plan(numeric_preset(options.num_preset))) {
-  spgemm_options o;
-  spgemm_options_default(&o);
-  std::snprintf(o.sym_preset, sizeof(o.sym_preset), "%s", options.sym_preset.c_str());
-  std::snprintf(o.num_preset, sizeof(o.num_preset), "%s", options.num_preset.c_str());
-  o.workers = options.workers;
-  o.overlap = options.overlap ? 1 : 0;
-  o.deterministic = options.deterministic ? 1 : 0;
-  o.chunk_rows = options.chunk_rows;
-  o.hash_scale = options.hash.hash_scale;
-  o.ordered_heap = options.ordered_heap ? 1 : 0;
-  if (options.sym_launch_order) {
-    o.has_sym_launch_order = 1;
-    std::copy(options.sym_launch_order->begin(), options.sym_launch_order->end(), o.sym_launch_order);
-  }
-  if (options.num_launch_order) {
-    o.has_num_launch_order = 1;
-    std::copy(options.num_launch_order->begin(), options.num_launch_order->end(), o.num_launch_order);
-  }
+  const spgemm_options o = to_c_options(options);
   if (a.cols != b.rows)
     throw std::invalid_argument("spgemm: a.cols (" + std::to_string(a.cols) + ") != b.rows (" +
                                 std::to_string(b.rows) + ")");
@@ -465,6 +470,50 @@ const BinningResult& SpgemmPipeline::binning() const {
   binning_.total_metric = info.total_metric;
   binning_.fast_path = info.fast_path != 0;
   return binning_;
+}
+
+SpgemmOutput multiply_multi(const CsrMatrix& a, const CsrMatrix& b, const SpgemmOptions& options,
+                            const std::vector<int>& devices) {
+  if (devices.empty()) throw std::invalid_argument("multiply_multi: no devices");
+  if (a.cols != b.rows)
+    throw std::invalid_argument("spgemm: a.cols (" + std::to_string(a.cols) + ") != b.rows (" +
+                                std::to_string(b.rows) + ")");
+  // one fresh context per entry (a context serves one host thread at a time)
+  std::vector<spgemm_ctx*> ctxs;
+  struct Release {
+    std::vector<spgemm_ctx*>& c;
+    ~Release() {
+      for (spgemm_ctx* x : c) spgemm_ctx_destroy(x);
+    }
+  } release{ctxs};
+  for (int d : devices) {
+    spgemm_ctx* c = nullptr;
+    ok(spgemm_ctx_create(d, &c));
+    ctxs.push_back(c);
+  }
+  const int n = static_cast<int>(ctxs.size());
+  const spgemm_options o = to_c_options(options);
+  const spgemm_csr_view va = view(a), vb = view(b);
+  std::vector<spgemm_matrix*> slices(static_cast<std::size_t>(n), nullptr);
+  std::vector<std::int64_t> bounds(static_cast<std::size_t>(n) + 1, 0);
+  spgemm_report r;
+  ok(spgemm_multiply_multi(ctxs.data(), n, &va, &vb, &o, slices.data(), bounds.data(), &r));
+  SpgemmOutput out;
+  out.c.rows = a.rows;
+  out.c.cols = b.cols;
+  out.c.rpt.resize(static_cast<std::size_t>(a.rows) + 1);
+  out.c.col.resize(static_cast<std::size_t>(r.nnz_of_product));
+  out.c.val.resize(static_cast<std::size_t>(r.nnz_of_product));
+  const spgemm_status st = spgemm_matrices_download_stitched(ctxs.data(), slices.data(), n, out.c.rpt.data(),
+                                                             out.c.col.data(), out.c.val.data());
+  for (spgemm_matrix* m : slices) spgemm_matrix_free(m);
+  ok(st);
+  out.stats = MatrixStats{r.rows, r.nnz, r.nnz_per_row_mean, r.max_nnz_per_row, r.total_nprod, r.nnz_of_product, r.cr};
+  out.timings = StepTimings{r.timings.setup,       r.timings.sym_binning, r.timings.symbolic, r.timings.rpt_alloc,
+                            r.timings.num_binning, r.timings.numeric,     r.timings.cleanup,  r.timings.total};
+  out.spilled_rows = r.spilled_rows;
+  out.workers = r.workers;
+  return out;
 }
 
 }  // namespace spgemm

@@ -133,3 +133,19 @@ def test_speculative_rows_mixed_with_abandoned(sg, oracle):
     assert_matches_oracle(out.c, exp, bitwise=True)
     nnz = np.diff(exp.rpt)
     assert (nnz[pick] <= 128).any() and (nnz[~pick] > 128).any()
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3])
+def test_multiply_multi_stitches_bitwise(sg, oracle, parts):
+    """spgemm_multiply_multi (SURVEY §8(e) inside one process): nprod-balanced row blocks
+    on separate contexts (here all on device 0, each on its own host thread), slices
+    stitched on the host -- bitwise the single-context product."""
+    from paper_2206_07244_b200.distributed import nprod_split
+    for a in (S.random_values(S.stencil3d_27pt(20), 6), S.random_values(S.rmat(12, 16, seed=12), 7)):
+        single = sg.multiply(a, a)
+        multi = sg.multiply_multi(a, a, devices=[0] * parts)
+        assert multi.c == single.c
+        assert multi.stats.total_nprod == single.stats.total_nprod
+        assert multi.stats.nnz_of_product == single.stats.nnz_of_product
+        nprod, _ = sg.compute_nprod(a, a)
+        assert multi.row_bounds == nprod_split(nprod, parts)
