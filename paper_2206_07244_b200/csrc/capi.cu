@@ -1072,7 +1072,11 @@ spgemm_status spgemm_pipeline_create(spgemm_ctx* ctx, const spgemm_csr_view* a,
         stage_input(ctx, b, &p->B, p->owned + 3, &p->b_nnz);
       }
       p->M = a->rows;
-      p->idx32 = p->a_nnz < (int64_t(1) << 31) && p->b_nnz < (int64_t(1) << 31);
+      // 32-bit B/A offsets in the group and heap kernels when every offset fits;
+      // SPGEMM_FORCE_IDX64=1 takes the 64-bit kernels regardless (test coverage of
+      // the path inputs above 2^31 nonzeros take)
+      p->idx32 = p->a_nnz < (int64_t(1) << 31) && p->b_nnz < (int64_t(1) << 31) &&
+                 std::getenv("SPGEMM_FORCE_IDX64") == nullptr;
       p->avg_b_len = b->rows > 0 ? static_cast<double>(p->b_nnz) / static_cast<double>(b->rows) : 0;
       for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     } catch (...) {
