@@ -643,11 +643,16 @@ def run_e2e(sg, torch, a_host, min_steps, device):
         return out.stats.total_nprod
 
     def step_sync():
+        t0 = time.perf_counter()
         p = sg.SpgemmPipeline(a, a, device=device)
         dm, out = p.run_device()
         p.close()
+        t1 = time.perf_counter()
         dm.download_into(orpt.numpy(), ocol.numpy(), oval.numpy())
         dm.free()
+        if os.environ.get("SPGEMM_BENCH_DEBUG"):
+            print(f"e2e sync run {1e3 * (t1 - t0):.2f} ms d2h {1e3 * (time.perf_counter() - t1):.2f} ms",
+                  file=sys.stderr)
         return out.stats.total_nprod
 
     dbg = os.environ.get("SPGEMM_BENCH_DEBUG")

@@ -185,6 +185,15 @@ struct spgemm_ctx {
   };
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
+  // Per-call scratch (the metadata arena, staged host inputs) kept across
+  // multiplies: re-allocating multi-GB arenas every call fragments the
+  // stream-ordered pool, whose growth then stalls a call for 100+ ms.
+  struct Scratch {
+    void* p;
+    size_t bytes;
+    bool busy;
+  };
+  std::vector<Scratch> scratch;
 };
 
 namespace {
@@ -290,6 +299,39 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
 
 void dev_free(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
+}
+
+// Scratch blocks live on the context and are used on its main stream only, so a
+// block released by one call and handed to the next is stream-ordered.
+void* scratch_acquire(spgemm_ctx* ctx, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  spgemm_ctx::Scratch* best = nullptr;
+  for (auto& b : ctx->scratch)
+    if (!b.busy && b.bytes >= bytes && b.bytes <= 2 * bytes + (size_t(64) << 20) && (!best || b.bytes < best->bytes))
+      best = &b;
+  if (best) {
+    best->busy = true;
+    return best->p;
+  }
+  // no fit: give the idle blocks back first, so the cache tracks the working set
+  std::vector<spgemm_ctx::Scratch> keep;
+  for (auto& b : ctx->scratch) {
+    if (b.busy) keep.push_back(b);
+    else dev_free(b.p, s);
+  }
+  ctx->scratch.swap(keep);
+  void* p = dev_alloc(bytes, s);
+  ctx->scratch.push_back({p, bytes, true});
+  return p;
+}
+
+void scratch_release(spgemm_ctx* ctx, void* p) {
+  if (!p) return;
+  for (auto& b : ctx->scratch)
+    if (b.p == p) {
+      b.busy = false;
+      return;
+    }
 }
 
 }  // namespace
@@ -402,9 +444,9 @@ void stage_input(spgemm_ctx* ctx, const spgemm_csr_view* v, DevCsr* d, void** ow
   const size_t rb = static_cast<size_t>(v->rows + 1) * sizeof(int64_t);
   const size_t cb = static_cast<size_t>(*nnz) * sizeof(int32_t);
   const size_t vb = static_cast<size_t>(*nnz) * sizeof(double);
-  owned[0] = dev_alloc(rb, ctx->main_s);
-  owned[1] = dev_alloc(cb, ctx->main_s);
-  owned[2] = dev_alloc(vb, ctx->main_s);
+  owned[0] = scratch_acquire(ctx, rb, ctx->main_s);
+  owned[1] = scratch_acquire(ctx, cb, ctx->main_s);
+  owned[2] = scratch_acquire(ctx, vb, ctx->main_s);
   ck(cudaMemcpyAsync(owned[0], v->rpt, rb, cudaMemcpyHostToDevice, ctx->main_s), "H2D rpt");
   if (cb) ck(cudaMemcpyAsync(owned[1], v->col, cb, cudaMemcpyHostToDevice, ctx->main_s), "H2D col");
   if (vb) ck(cudaMemcpyAsync(owned[2], v->val, vb, cudaMemcpyHostToDevice, ctx->main_s), "H2D val");
@@ -464,7 +506,7 @@ void spgemm_pipeline::setup() {
   const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
   if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
   arena_bytes = off;
-  d_arena = static_cast<unsigned char*>(dev_alloc(arena_bytes, s));
+  d_arena = static_cast<unsigned char*>(scratch_acquire(ctx, arena_bytes, s));
   metadata_calls += 1;
   metadata_bytes += static_cast<int64_t>(arena_bytes);
   d_flags = reinterpret_cast<int*>(d_arena + o_flags);
@@ -840,7 +882,7 @@ void spgemm_pipeline::finish(spgemm_report* r) {
   // Cleanup: the metadata arena goes only now, after every kernel of both
   // phases (pipeline.cpp:449-455).
   const auto t0 = std::chrono::steady_clock::now();
-  dev_free(d_arena, ctx->main_s);
+  scratch_release(ctx, d_arena);
   d_arena = nullptr;
   rep.timings.cleanup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   rep.timings.total = rep.timings.setup + rep.timings.sym_binning + rep.timings.symbolic +
@@ -861,10 +903,10 @@ void spgemm_pipeline::release(bool keep_result) {
     alloc_pending = false;
   }
   for (void*& p : owned) {
-    dev_free(p, s);
+    scratch_release(ctx, p);
     p = nullptr;
   }
-  dev_free(d_arena, s);
+  scratch_release(ctx, d_arena);
   d_arena = nullptr;
   if (!keep_result) {
     dev_free(d_rpt, s);
@@ -958,6 +1000,7 @@ void spgemm_ctx_destroy(spgemm_ctx* c) {
     cudaEventDestroy(r.b);
   }
   for (auto& e : c->ev_pool) cudaEventDestroy(e);
+  for (auto& b : c->scratch) cudaFree(b.p);
   if (c->h_info) cudaFreeHost(c->h_info);
   if (prev >= 0) cudaSetDevice(prev);
   delete c;
