@@ -157,6 +157,11 @@ BinUpper to_upper(const spgemm_bin_config& c) {
 }
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+#ifndef SPGEMM_G8_MAX
+#define SPGEMM_G8_MAX 8.0
+#endif
+// 8-lane groups when B's rows average at most this many entries (else 32)
+constexpr double kG8MaxBLen = SPGEMM_G8_MAX;
 constexpr int kSpecCap = 128;                          // entries per row of the speculative scratch
 constexpr int64_t kSpecBudget = int64_t(4) << 30;      // scratch bytes the arena may spend on it
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -560,7 +565,7 @@ void spgemm_pipeline::symbolic_binning() {
 
 void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s) {
   const int64_t u = sym_plan.config.upper[bin];
-  const bool g8 = avg_b_len <= 8.0;
+  const bool g8 = avg_b_len <= kG8MaxBLen;
   auto group = [&](auto kern, int G, int T, int NGRP, int WB) {
     // Only where the numeric phase would also run a 32-lane group on a table
     // of 256 (rows with 513..1024 products, or 257..512 when B's rows average
@@ -755,7 +760,7 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
                                      double* gvals, uint32_t* gbits, int64_t gslots,
                                      int64_t gwords, int gblocks) {
   const int64_t u = num_plan.config.upper[bin];
-  const bool g8 = avg_b_len <= 8.0;
+  const bool g8 = avg_b_len <= kG8MaxBLen;
   auto group = [&](auto kern, int G, int T, int E, int NGRP) {
     const size_t smem = static_cast<size_t>(NGRP) * ((T + 2) * 8 + G * E * 8 + T * 4 + G * 16 + 16);
     prepare_kernel(ctx, kern, smem);
