@@ -1,5 +1,6 @@
 """Drop-in proof: the REFERENCE's own unit tests (proj/tests/test_pipeline.cpp,
-test_binning.cpp, test_csr.cpp), compiled unmodified and in place against this repo's
+test_binning.cpp, test_csr.cpp, test_bench.cpp -- the last runs the reference's bench.cpp
+run_benchmark over this library), compiled unmodified and in place against this repo's
 C++ headers (include/spgemm/*.hpp) and libspgemm_b200.so by tests/cpp/Makefile.
 The binaries are built in the build container (where /root/reference exists) and
 travel with the repo snapshot; the tests skip when they are absent."""
@@ -26,7 +27,7 @@ def test_reference_test_csr_host():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["test_pipeline", "test_binning"])
+@pytest.mark.parametrize("name", ["test_pipeline", "test_binning", "test_bench"])
 def test_reference_unit_tests_on_b200(name):
     res, failed = _run(name)
     assert res.returncode == 0 and not failed, res.stdout[-4000:]
