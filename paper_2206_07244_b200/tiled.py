@@ -111,36 +111,53 @@ def _tile_checksum(dm, row0: int, col0: int):
 
 def stream_multiply(a: CsrMatrix, b: CsrMatrix, rows: Optional[range] = None, nprod: Optional[np.ndarray] = None,
                     budget: int = 4_000_000_000, window: int = WINDOW, b_windows: Optional[List[CsrMatrix]] = None,
-                    device: Optional[int] = None, options=None) -> StreamReport:
+                    device: Optional[int] = None, options=None, workers: int = 1) -> StreamReport:
     """C = A[rows].B computed tile by tile (row blocks x column windows) and
     streamed into checksums. A row block holds at most ``budget`` products over
     all windows, so no tile's C exceeds 12 * budget bytes. ``nprod`` (per row of
-    A, from K1) and ``b_windows`` can be passed in to share them across calls."""
+    A, from K1) and ``b_windows`` can be passed in to share them across calls.
+
+    ``workers`` > 1 runs that many tiles at once, each on its own host thread
+    and context (streams): the SMs a tile leaves idle while its heaviest rows
+    finish (R-MAT hubs) are taken by the next tile."""
     if nprod is None:
         nprod, _ = compute_nprod(a, b, device=device)
     nprod = np.asarray(nprod, np.int64)
     r_lo, r_hi = (0, a.rows) if rows is None else (rows.start, rows.stop)
     wins = b_windows if b_windows is not None else split_columns(b, window)
-    rep = StreamReport()
     bounds = row_blocks(nprod[r_lo:r_hi], max(1, budget))
+    tiles = []
     for i in range(len(bounds) - 1):
         r0, r1 = r_lo + bounds[i], r_lo + bounds[i + 1]
-        if r1 <= r0:
-            continue
-        a_blk = _slice_rows_dev(a, r0, r1)
-        for w, bw in enumerate(wins):
-            dm, out = multiply_device(a_blk, bw, options, device=device)
-            try:
-                s, h = _tile_checksum(dm, r0, w * window)
-                rep.total_nprod += out.stats.total_nprod
-                rep.tile_nprod.append(out.stats.total_nprod)
-                rep.nnz += out.stats.nnz_of_product
-                rep.val_sum += s
-                rep.pattern_hash = (rep.pattern_hash + h) & ((1 << 64) - 1)
-                rep.spilled_rows += out.spilled_rows
-                rep.tiles += 1
-            finally:
-                dm.free()
+        if r1 > r0:
+            tiles.extend((r0, r1, w) for w in range(len(wins)))
+
+    def run_tile(t):
+        r0, r1, w = t
+        if device is not None:
+            _torch().cuda.set_device(device)
+        dm, out = multiply_device(_slice_rows_dev(a, r0, r1), wins[w], options, device=device)
+        try:
+            s, h = _tile_checksum(dm, r0, w * window)
+            return out.stats.total_nprod, out.stats.nnz_of_product, s, h, out.spilled_rows
+        finally:
+            dm.free()
+
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            results = list(ex.map(run_tile, tiles))
+    else:
+        results = [run_tile(t) for t in tiles]
+    rep = StreamReport()
+    for np_t, nnz_t, s, h, spilled in results:
+        rep.total_nprod += np_t
+        rep.tile_nprod.append(np_t)
+        rep.nnz += nnz_t
+        rep.val_sum += s
+        rep.pattern_hash = (rep.pattern_hash + h) & ((1 << 64) - 1)
+        rep.spilled_rows += spilled
+        rep.tiles += 1
     return rep
 
 

@@ -11,13 +11,14 @@ from paper_2206_07244_b200 import tiled as T
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("window,budget", [(4096, 2_000_000), (1 << 20, 10**12), (1000, 500_000)])
-def test_stream_matches_untiled(sg, window, budget):
+@pytest.mark.parametrize("window,budget,workers", [(4096, 2_000_000, 1), (1 << 20, 10**12, 1),
+                                                   (1000, 500_000, 1), (4096, 2_000_000, 3)])
+def test_stream_matches_untiled(sg, window, budget, workers):
     a = S.random_values(S.rmat(13, 16, seed=13), 7)
     full = sg.multiply(a, a).c
     ref = T.checksum_of(full)
     d = a.to_device()
-    rep = T.stream_multiply(d, d, budget=budget, window=window)
+    rep = T.stream_multiply(d, d, budget=budget, window=window, workers=workers)
     assert rep.total_nprod == sg.compute_nprod(a, a)[1]
     assert rep.nnz == ref.nnz
     assert rep.pattern_hash == ref.pattern_hash
