@@ -546,18 +546,18 @@ def run_config5(args):
     tw0 = time.time()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    launches0 = ctx.kernel_launches
+    launches = 0
     nprod_done = 0
     for _ in range(args.steps):
         rep = step()
         nprod_done += rep.total_nprod
+        launches += rep.kernel_launches
     ev1.record(stream)
     torch.cuda.synchronize()
     tw1 = time.time()
     if rank == 0:
         clocks.stop()
     t_ms = ev0.elapsed_time(ev1)
-    launches = ctx.kernel_launches - launches0
     if dist:
         dist.barrier()
         tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")

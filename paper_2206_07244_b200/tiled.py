@@ -27,7 +27,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .api import CsrMatrix, compute_nprod, multiply_device
+from .api import CsrMatrix, compute_nprod, get_context, multiply_device
 
 WINDOW = 1 << 20
 
@@ -102,6 +102,7 @@ class StreamReport:
     pattern_hash: int = 0
     tiles: int = 0
     spilled_rows: int = 0
+    kernel_launches: int = 0  # summed over the tiles' contexts (each worker thread has its own)
     tile_nprod: List[int] = field(default_factory=list)
 
 
@@ -136,10 +137,12 @@ def stream_multiply(a: CsrMatrix, b: CsrMatrix, rows: Optional[range] = None, np
         r0, r1, w = t
         if device is not None:
             _torch().cuda.set_device(device)
+        ctx = get_context(device)
+        l0 = ctx.kernel_launches
         dm, out = multiply_device(_slice_rows_dev(a, r0, r1), wins[w], options, device=device)
         try:
             s, h = _tile_checksum(dm, r0, w * window)
-            return out.stats.total_nprod, out.stats.nnz_of_product, s, h, out.spilled_rows
+            return out.stats.total_nprod, out.stats.nnz_of_product, s, h, out.spilled_rows, ctx.kernel_launches - l0
         finally:
             dm.free()
 
@@ -150,7 +153,8 @@ def stream_multiply(a: CsrMatrix, b: CsrMatrix, rows: Optional[range] = None, np
     else:
         results = [run_tile(t) for t in tiles]
     rep = StreamReport()
-    for np_t, nnz_t, s, h, spilled in results:
+    for np_t, nnz_t, s, h, spilled, nl in results:
+        rep.kernel_launches += nl
         rep.total_nprod += np_t
         rep.tile_nprod.append(np_t)
         rep.nnz += nnz_t

@@ -25,6 +25,8 @@ def test_stream_matches_untiled(sg, window, budget, workers):
     assert abs(rep.val_sum - ref.val_sum) <= 1e-9 * max(1.0, abs(ref.val_sum))
     if window < a.cols:
         assert rep.tiles > 1
+    # every tile ran the native kernels (>= K1, scan, one symbolic and numeric launch, checksum)
+    assert rep.kernel_launches >= 4 * rep.tiles
 
 
 def test_split_columns_partition(sg):
