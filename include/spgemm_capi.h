@@ -226,6 +226,23 @@ spgemm_status spgemm_multiply_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_c
 spgemm_status spgemm_matrices_download_stitched(spgemm_ctx** ctxs, spgemm_matrix* const* slices, int32_t n,
                                                 int64_t* rpt, int32_t* col, double* val);
 
+/* ------------------------------------------------ symbolic-only sizing */
+/* B200 extension: nnz(C) without computing or
+ * allocating C -- the reference's step API run as setup + symbolic_binning +
+ * run_symbolic and the row_ptr region read back (pipeline.cpp:152-239,
+ * pipeline.hpp:190-201), here as one call. row_nnz (host, rows entries, may be
+ * NULL) receives nnz(C(i,:)); total_nnz / total_nprod (may be NULL) the sums.
+ * Device memory: the pipeline's O(rows) metadata only, so products whose C
+ * exceeds HBM (BASELINE config 5) can be sized before they are committed. */
+spgemm_status spgemm_forecast_nnz(spgemm_ctx* ctx, const spgemm_csr_view* a, const spgemm_csr_view* b,
+                                  const spgemm_options* opts, int64_t* row_nnz, int64_t* total_nnz,
+                                  int64_t* total_nprod);
+/* The same over n contexts: rows split as in spgemm_multiply_multi (row_bounds
+ * may be NULL), one host thread per context, host-resident operands. */
+spgemm_status spgemm_forecast_nnz_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_csr_view* a,
+                                        const spgemm_csr_view* b, const spgemm_options* opts, int64_t* row_nnz,
+                                        int64_t* row_bounds, int64_t* total_nnz, int64_t* total_nprod);
+
 /* ----------------------------------------------- standalone GPU kernels */
 /* compute_nprod() (reference.cpp:37-55) on the device: out[M] host or device. */
 spgemm_status spgemm_compute_nprod(spgemm_ctx* ctx, const spgemm_csr_view* a,

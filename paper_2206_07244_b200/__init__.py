@@ -5,8 +5,9 @@ The product is the sm_100a library ``lib/libspgemm_b200.so`` behind the C ABI in
 """
 from .api import (  # noqa: F401
     AllocStats, BinConfig, BinningResult, BinStrategy, Context, CsrMatrix, CudaError, DeviceMatrix,
-    ExecutionPlan, InvalidArgument, LogicError, MatrixStats, NoDevice, SpgemmOptions, SpgemmOutput,
-    SpgemmPipeline, StepTimings, SYMBOLIC, NUMERIC, build_rpt, classify, compute_nprod, get_context,
+    ExecutionPlan, InvalidArgument, LogicError, MatrixStats, NnzForecast, NoDevice, SpgemmOptions, SpgemmOutput,
+    SpgemmPipeline, StepTimings, SYMBOLIC, NUMERIC, build_rpt, classify, compute_nprod, forecast_nnz,
+    forecast_nnz_multi, get_context,
     kDefaultNumPreset, kDefaultSymPreset, kMaxSymbolicTableSize, kNoUpperBound, kNumBins,
     kSymbolicSpillThreshold, make_execution_plan, max_relative_error, multiply, multiply_device,
     multiply_multi, numeric_preset, preset, preset_names, run_binning, same_pattern, symbolic_preset, validate_csr,

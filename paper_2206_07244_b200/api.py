@@ -756,6 +756,72 @@ def multiply_multi(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] 
     return out
 
 
+@dataclass
+class NnzForecast:
+    """Symbolic-only sizing of C = A*B."""
+    rows: int
+    total_nnz: int
+    total_nprod: int
+    row_nnz: Optional[np.ndarray] = None      # nnz(C(i,:)) per row, when asked for
+    row_bounds: Optional[List[int]] = None    # the row split (forecast_nnz_multi)
+
+    @property
+    def cr(self) -> float:
+        """Compression ratio nprod / nnz(C) (pipeline.hpp SpgemmStats::cr)."""
+        return self.total_nprod / self.total_nnz if self.total_nnz else 0.0
+
+    @property
+    def c_bytes(self) -> int:
+        """Bytes C will take as CSR (int64 rpt, int32 col, fp64 val)."""
+        return 8 * (self.rows + 1) + 12 * self.total_nnz
+
+
+def forecast_nnz(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] = None,
+                 device: Optional[int] = None, per_row: bool = True) -> NnzForecast:
+    """nnz(C) without computing or allocating C (C ABI spgemm_forecast_nnz): the
+    reference's setup + symbolic_binning + run_symbolic + row_ptr region
+    (pipeline.cpp:152-239) in one call, O(rows) device memory."""
+    if a.cols != b.rows:
+        raise InvalidArgument("forecast_nnz: a.cols != b.rows")
+    rows = np.empty(a.rows, np.int64) if per_row else None
+    tn, tp = C.c_int64(), C.c_int64()
+    va, vb = a._view(), b._view()
+    opts = options._c() if options is not None else None
+    _check(_c.lib.spgemm_forecast_nnz(get_context(device).handle, C.byref(va), C.byref(vb),
+                                      C.byref(opts) if opts is not None else None,
+                                      rows.ctypes.data if per_row and a.rows else None, C.byref(tn), C.byref(tp)))
+    return NnzForecast(a.rows, int(tn.value), int(tp.value), rows)
+
+
+def forecast_nnz_multi(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] = None,
+                       devices: Sequence[int] = (0,), per_row: bool = True) -> NnzForecast:
+    """forecast_nnz over several devices in one process (spgemm_forecast_nnz_multi):
+    the nprod-balanced row split of multiply_multi, each block counted on its own
+    device and host thread."""
+    devices = list(devices)
+    if not devices:
+        raise InvalidArgument("forecast_nnz_multi: no devices")
+    if a.cols != b.rows:
+        raise InvalidArgument("forecast_nnz_multi: a.cols != b.rows")
+    ctxs = [Context(d) for d in devices]
+    n = len(ctxs)
+    handles = (C.c_void_p * n)(*[c.handle for c in ctxs])
+    bounds = (C.c_int64 * (n + 1))()
+    rows = np.empty(a.rows, np.int64) if per_row else None
+    tn, tp = C.c_int64(), C.c_int64()
+    va, vb = a._view(), b._view()
+    opts = options._c() if options is not None else None
+    try:
+        _check(_c.lib.spgemm_forecast_nnz_multi(handles, n, C.byref(va), C.byref(vb),
+                                                C.byref(opts) if opts is not None else None,
+                                                rows.ctypes.data if per_row and a.rows else None, bounds,
+                                                C.byref(tn), C.byref(tp)))
+    finally:
+        for c in ctxs:
+            c.close()
+    return NnzForecast(a.rows, int(tn.value), int(tp.value), rows, [int(x) for x in bounds])
+
+
 def multiply_device(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] = None,
                     device: Optional[int] = None):
     """C = A*B with C left in HBM. Returns (DeviceMatrix, SpgemmOutput with c=None)."""

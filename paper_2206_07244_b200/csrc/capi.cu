@@ -375,6 +375,7 @@ struct spgemm_pipeline {
   int64_t* d_spill = nullptr;
   Spec spec{nullptr, nullptr, nullptr, 0};  // speculative numeric scratch (arena)
   bool regular_a = false;                    // A's longest row <= 4x its mean (set by setup)
+  bool symbolic_only = false;                // spgemm_forecast_nnz: no speculative numeric, no C
   int32_t* d_blk = nullptr;
   int* d_flags = nullptr;
   long long* d_sums = nullptr;
@@ -506,7 +507,7 @@ void spgemm_pipeline::setup() {
   off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
   regular_a = M > 0 && static_cast<double>(h_sym.a_max_row) <= 4.0 * static_cast<double>(a_nnz) / static_cast<double>(M);
   const bool use_spec = idx32 && M > 0 && avg_b_len > 8.0 && regular_a && M * kSpecCap * 12 <= kSpecBudget &&
-                        std::getenv("SPGEMM_NO_SPEC") == nullptr;
+                        !symbolic_only && std::getenv("SPGEMM_NO_SPEC") == nullptr;
   const size_t o_sflag = off, o_scol = align_up(o_sflag + (use_spec ? static_cast<size_t>(M) : 0), 256);
   const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
   if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
@@ -716,7 +717,7 @@ void spgemm_pipeline::numeric_binning() {
   if (h_num.total > static_cast<unsigned long long>(std::numeric_limits<int64_t>::max()))
     fail(SPGEMM_OVERFLOW, "spgemm: nonzero count overflowed 64 bits");
   total_nnz = static_cast<int64_t>(h_num.total);
-  if (opts.overlap) {
+  if (opts.overlap && !symbolic_only) {
     // C.col/C.val are allocated now, stream-ordered behind the scatter that is
     // still running (the allocation lane of pipeline.cpp:254-257). Same stream
     // as the previous product's free, so the pool reuses that memory directly.
@@ -1393,6 +1394,35 @@ spgemm_status spgemm_compute_nprod(spgemm_ctx* ctx, const spgemm_csr_view* a,
   st = spgemm_pipeline_setup(p);
   if (st == SPGEMM_OK && out_host) st = spgemm_pipeline_rpt_region(p, out_host);
   if (st == SPGEMM_OK && total) *total = p->total_nprod;
+  std::string keep = g_err;
+  spgemm_pipeline_destroy(p);
+  g_err = keep;
+  return st;
+}
+
+spgemm_status spgemm_forecast_nnz(spgemm_ctx* ctx, const spgemm_csr_view* a, const spgemm_csr_view* b,
+                                  const spgemm_options* opts, int64_t* row_nnz, int64_t* total_nnz,
+                                  int64_t* total_nprod) {
+  spgemm_pipeline* p = nullptr;
+  spgemm_status st = spgemm_pipeline_create(ctx, a, b, opts, &p);
+  if (st != SPGEMM_OK) return st;
+  st = guard([&] {
+    DeviceGuard g(p->ctx->device);
+    p->symbolic_only = true;
+    p->setup();
+    p->symbolic_binning();
+    p->run_symbolic();
+    // per-row counts are in the C.rpt block now; the numeric pass 1 sums them
+    // on the device (no C allocation when symbolic_only)
+    if (row_nnz && p->M > 0)
+      ck(cudaMemcpyAsync(row_nnz, p->d_rpt, static_cast<size_t>(p->M) * 8, cudaMemcpyDeviceToHost,
+                         p->ctx->main_s),
+         "D2H row nnz");
+    p->numeric_binning();
+    ck(cudaStreamSynchronize(p->ctx->main_s), "cudaStreamSynchronize");
+    if (total_nnz) *total_nnz = p->total_nnz;
+    if (total_nprod) *total_nprod = p->total_nprod;
+  });
   std::string keep = g_err;
   spgemm_pipeline_destroy(p);
   g_err = keep;

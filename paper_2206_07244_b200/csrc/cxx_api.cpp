@@ -516,4 +516,33 @@ SpgemmOutput multiply_multi(const CsrMatrix& a, const CsrMatrix& b, const Spgemm
   return out;
 }
 
+NnzForecast forecast_nnz(const CsrMatrix& a, const CsrMatrix& b, const SpgemmOptions& options,
+                         const std::vector<int>& devices, bool per_row) {
+  if (devices.empty()) throw std::invalid_argument("forecast_nnz: no devices");
+  if (a.cols != b.rows)
+    throw std::invalid_argument("spgemm: a.cols (" + std::to_string(a.cols) + ") != b.rows (" +
+                                std::to_string(b.rows) + ")");
+  std::vector<spgemm_ctx*> ctxs;
+  struct Release {
+    std::vector<spgemm_ctx*>& c;
+    ~Release() {
+      for (spgemm_ctx* x : c) spgemm_ctx_destroy(x);
+    }
+  } release{ctxs};
+  for (int d : devices) {
+    spgemm_ctx* c = nullptr;
+    ok(spgemm_ctx_create(d, &c));
+    ctxs.push_back(c);
+  }
+  const int n = static_cast<int>(ctxs.size());
+  const spgemm_options o = to_c_options(options);
+  const spgemm_csr_view va = view(a), vb = view(b);
+  NnzForecast f;
+  if (per_row) f.row_nnz.resize(static_cast<std::size_t>(a.rows));
+  f.row_bounds.resize(static_cast<std::size_t>(n) + 1);
+  ok(spgemm_forecast_nnz_multi(ctxs.data(), n, &va, &vb, &o, per_row && a.rows ? f.row_nnz.data() : nullptr,
+                               f.row_bounds.data(), &f.total_nnz, &f.total_nprod));
+  return f;
+}
+
 }  // namespace spgemm

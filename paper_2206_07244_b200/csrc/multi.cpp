@@ -10,6 +10,9 @@
 //   3. C stays distributed as one device-resident slice per device; the row
 //      pointers are stitched from the slices' nnz totals when C is downloaded
 //      (spgemm_matrices_download_stitched) -- no further exchange.
+//   4. symbolic-only sizing (spgemm_forecast_nnz_multi):
+//      the same split, every device counting its block's nnz(C) without
+//      allocating C, so a TB-scale product is sized before it is committed.
 //
 // The torch.distributed path (paper_2206_07244_b200/distributed.py) is the same
 // decomposition with one process per GPU and an NCCL broadcast of B.
@@ -34,6 +37,46 @@ struct Block {
   spgemm_report report{};
 };
 
+// nprod (K1 on ctxs[0]) and the balanced contiguous row split into row_bounds[0..n]
+spgemm_status split_rows(spgemm_ctx* ctx, int32_t n, const spgemm_csr_view* a, const spgemm_csr_view* b,
+                         int64_t* row_bounds) {
+  std::vector<int64_t> nprod(static_cast<size_t>(std::max<int64_t>(a->rows, 0)));
+  int64_t total = 0;
+  spgemm_status st = spgemm_compute_nprod(ctx, a, b, nprod.data(), &total);
+  if (st != SPGEMM_OK) return st;
+  row_bounds[0] = 0;
+  int64_t acc = 0, row = 0;
+  for (int32_t g = 1; g < n; ++g) {
+    const int64_t target = total > 0 ? static_cast<int64_t>((static_cast<__int128>(total) * g) / n) : 0;
+    // first row whose exclusive prefix reaches the target
+    while (row < a->rows && acc < target) acc += nprod[static_cast<size_t>(row++)];
+    row_bounds[g] = total > 0 ? row : (a->rows * g) / n;
+    if (row_bounds[g] < row_bounds[g - 1]) row_bounds[g] = row_bounds[g - 1];
+  }
+  row_bounds[n] = a->rows;
+  return SPGEMM_OK;
+}
+
+// rows [r0, r1) of a host CSR view, row pointers rebased into bl.rpt
+void make_block(const spgemm_csr_view* a, int64_t r0, int64_t r1, Block& bl) {
+  bl.r0 = r0;
+  bl.r1 = r1;
+  const int64_t p0 = a->rpt[r0];
+  bl.rpt.resize(static_cast<size_t>(r1 - r0 + 1));
+  for (int64_t r = r0; r <= r1; ++r) bl.rpt[static_cast<size_t>(r - r0)] = a->rpt[r] - p0;
+  bl.view = spgemm_csr_view{r1 - r0, a->cols, bl.rpt.data(), a->col ? a->col + p0 : nullptr,
+                            a->val ? a->val + p0 : nullptr, 0};
+}
+
+// runs work(i) for i in [0, n): i = 0 on the calling thread, the rest on their own
+template <typename F>
+void run_parallel(int32_t n, F work) {
+  std::vector<std::thread> threads;
+  for (int32_t i = 1; i < n; ++i) threads.emplace_back(work, i);
+  work(0);
+  for (auto& t : threads) t.join();
+}
+
 }  // namespace
 
 extern "C" {
@@ -55,43 +98,16 @@ spgemm_status spgemm_multiply_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_c
   }
   if (a->cols != b->rows) return SPGEMM_INVALID_ARGUMENT;
   // 1. nprod per row (K1) and the balanced split
-  std::vector<int64_t> nprod(static_cast<size_t>(std::max<int64_t>(a->rows, 0)));
-  int64_t total = 0;
-  spgemm_status st = spgemm_compute_nprod(ctxs[0], a, b, nprod.data(), &total);
+  spgemm_status st = split_rows(ctxs[0], n, a, b, row_bounds);
   if (st != SPGEMM_OK) return st;
-  row_bounds[0] = 0;
-  {
-    int64_t acc = 0, row = 0;
-    for (int32_t g = 1; g < n; ++g) {
-      const int64_t target = total > 0 ? static_cast<int64_t>((static_cast<__int128>(total) * g) / n) : 0;
-      // first row whose exclusive prefix reaches the target
-      while (row < a->rows && acc < target) acc += nprod[static_cast<size_t>(row++)];
-      row_bounds[g] = total > 0 ? row : (a->rows * g) / n;
-      if (row_bounds[g] < row_bounds[g - 1]) row_bounds[g] = row_bounds[g - 1];
-    }
-    row_bounds[n] = a->rows;
-  }
   // 2. one host thread per device
   std::vector<Block> blocks(static_cast<size_t>(n));
-  for (int32_t i = 0; i < n; ++i) {
-    Block& bl = blocks[static_cast<size_t>(i)];
-    bl.r0 = row_bounds[i];
-    bl.r1 = row_bounds[i + 1];
-    const int64_t p0 = a->rpt[bl.r0];
-    bl.rpt.resize(static_cast<size_t>(bl.r1 - bl.r0 + 1));
-    for (int64_t r = bl.r0; r <= bl.r1; ++r) bl.rpt[static_cast<size_t>(r - bl.r0)] = a->rpt[r] - p0;
-    bl.view = spgemm_csr_view{bl.r1 - bl.r0, a->cols, bl.rpt.data(), a->col ? a->col + p0 : nullptr,
-                              a->val ? a->val + p0 : nullptr, 0};
-  }
-  auto work = [&](int32_t i) {
+  for (int32_t i = 0; i < n; ++i) make_block(a, row_bounds[i], row_bounds[i + 1], blocks[static_cast<size_t>(i)]);
+  run_parallel(n, [&](int32_t i) {
     Block& bl = blocks[static_cast<size_t>(i)];
     bl.status = spgemm_multiply(ctxs[i], &bl.view, b, opts, &slices[i], &bl.report);
     if (bl.status != SPGEMM_OK) bl.error = spgemm_last_error();
-  };
-  std::vector<std::thread> threads;
-  for (int32_t i = 1; i < n; ++i) threads.emplace_back(work, i);
-  work(0);
-  for (auto& t : threads) t.join();
+  });
   for (int32_t i = 0; i < n; ++i) {
     const Block& bl = blocks[static_cast<size_t>(i)];
     if (bl.status != SPGEMM_OK) {
@@ -144,6 +160,48 @@ spgemm_status spgemm_matrices_download_stitched(spgemm_ctx** ctxs, spgemm_matrix
     row += rows;
     off += nnz;
   }
+  return SPGEMM_OK;
+}
+
+spgemm_status spgemm_forecast_nnz_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_csr_view* a,
+                                        const spgemm_csr_view* b, const spgemm_options* opts, int64_t* row_nnz,
+                                        int64_t* row_bounds, int64_t* total_nnz, int64_t* total_nprod) {
+  if (n < 1 || !ctxs || !a || !b) return SPGEMM_INVALID_ARGUMENT;
+  if (n == 1) {
+    if (row_bounds) {
+      row_bounds[0] = 0;
+      row_bounds[1] = a->rows;
+    }
+    return spgemm_forecast_nnz(ctxs[0], a, b, opts, row_nnz, total_nnz, total_nprod);
+  }
+  if (a->on_device || b->on_device) return SPGEMM_INVALID_ARGUMENT;
+  if (a->cols != b->rows) return SPGEMM_INVALID_ARGUMENT;
+  std::vector<int64_t> bounds(static_cast<size_t>(n) + 1);
+  spgemm_status st = split_rows(ctxs[0], n, a, b, bounds.data());
+  if (st != SPGEMM_OK) return st;
+  if (row_bounds) std::copy(bounds.begin(), bounds.end(), row_bounds);
+  std::vector<Block> blocks(static_cast<size_t>(n));
+  std::vector<int64_t> nnz(static_cast<size_t>(n), 0), np(static_cast<size_t>(n), 0);
+  for (int32_t i = 0; i < n; ++i) make_block(a, bounds[i], bounds[i + 1], blocks[static_cast<size_t>(i)]);
+  run_parallel(n, [&](int32_t i) {
+    Block& bl = blocks[static_cast<size_t>(i)];
+    if (bl.r1 == bl.r0) return;
+    bl.status = spgemm_forecast_nnz(ctxs[i], &bl.view, b, opts, row_nnz ? row_nnz + bl.r0 : nullptr,
+                                    &nnz[static_cast<size_t>(i)], &np[static_cast<size_t>(i)]);
+    if (bl.status != SPGEMM_OK) bl.error = spgemm_last_error();
+  });
+  int64_t tn = 0, tp = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const Block& bl = blocks[static_cast<size_t>(i)];
+    if (bl.status != SPGEMM_OK) {
+      spgemm_internal_set_error(("device block " + std::to_string(i) + ": " + bl.error).c_str());
+      return bl.status;
+    }
+    tn += nnz[static_cast<size_t>(i)];
+    tp += np[static_cast<size_t>(i)];
+  }
+  if (total_nnz) *total_nnz = tn;
+  if (total_nprod) *total_nprod = tp;
   return SPGEMM_OK;
 }
 

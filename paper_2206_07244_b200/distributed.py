@@ -10,7 +10,14 @@ gloo in the CPU tests). The only exchange is the replication of B:
    collective needed for the partition;
 3. each rank multiplies its contiguous row block A[r0:r1, :] by B independently;
 4. row pointers are stitched from the per-rank nnz totals (one all-gather of G
-   int64 values); C stays distributed unless the caller asks for it on one rank.
+   int64 values); C stays distributed unless the caller asks for it on one rank
+   (``gather_csr``: point-to-point transfers of each slice's arrays to that rank,
+   assembled into one host CSR -- SURVEY.md §8(f) item 4).
+
+``forecast_distributed`` is the symbolic-only variant (§8(f) item 4): the same
+broadcast and split, every rank counting its block's nnz(C) without allocating
+C, the totals combined with one all-reduce -- sizing a TB-scale product (config
+5) before committing memory to it.
 
 The local multiply / nprod functions default to the B200 library; the CPU tests
 inject the oracle to exercise the partition/broadcast/stitch logic with gloo.
@@ -140,9 +147,97 @@ def multiply_distributed(a: Optional[CsrMatrix], b: Optional[CsrMatrix], *, same
     offsets = [int(x) for x in np.concatenate([[0], np.cumsum(nnzs)[:-1]])]
     res = DistributedResult(c_loc, bounds, offsets, int(nprod.sum()))
     if gather_to is not None:
-        parts = [None] * world
-        h = c_loc.to_host()
-        dist.all_gather_object(parts, (h.rows, h.cols, h.rpt, h.col, h.val), group=group)
-        if rank == gather_to:
-            res.c = stitch([CsrMatrix(*p) for p in parts], B.cols)
+        res.c = gather_csr(c_loc, gather_to, device=device, group=group)
     return res
+
+
+def gather_csr(c_local: CsrMatrix, dst: int = 0, device=None, group=None) -> Optional[CsrMatrix]:
+    """Assemble the ranks' row blocks of C (in rank order) into one host CSR on rank
+    ``dst`` (None elsewhere). The block sizes travel in one all-gather; every other
+    rank then sends its rpt/col/val with point-to-point transfers (NCCL from HBM on
+    the GPU box, gloo on CPU), received one block at a time so ``dst`` needs device
+    room for the largest block only. Row pointers are rebased by the nnz offsets."""
+    import torch
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    mine = torch.tensor([c_local.rows, c_local.nnz()], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, mine, group=group)
+    sizes = [(int(t[0]), int(t[1])) for t in sizes]
+
+    def tensors(m: CsrMatrix):
+        if m.on_device and dev.type == "cuda":
+            return m.rpt, m.col, m.val
+        h = m.to_host()
+        return tuple(torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (h.rpt, h.col, h.val))
+
+    if rank != dst:
+        for t in tensors(c_local):
+            if t.numel():
+                dist.send(t.contiguous(), dst, group=group)
+        return None
+    rows = sum(r for r, _ in sizes)
+    nnz = sum(n for _, n in sizes)
+    rpt = np.empty(rows + 1, np.int64)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float64)
+    rpt[0] = 0
+    r0 = off = 0
+    for g, (rg, ng) in enumerate(sizes):
+        if g == rank:
+            h = c_local.to_host()
+            brpt, bcol, bval = np.asarray(h.rpt), np.asarray(h.col), np.asarray(h.val)
+        else:
+            ts = [torch.empty(rg + 1, dtype=torch.int64, device=dev), torch.empty(ng, dtype=torch.int32, device=dev),
+                  torch.empty(ng, dtype=torch.float64, device=dev)]
+            for t in ts:
+                if t.numel():
+                    dist.recv(t, g, group=group)
+            brpt, bcol, bval = (t.cpu().numpy() for t in ts)
+        rpt[r0 + 1:r0 + rg + 1] = brpt[1:] + off
+        col[off:off + ng] = bcol
+        val[off:off + ng] = bval
+        r0 += rg
+        off += ng
+    return CsrMatrix(rows, c_local.cols, rpt, col, val)
+
+
+@dataclass
+class DistributedForecast:
+    total_nnz: int              # nnz(C) of the whole product (all-reduced)
+    total_nprod: int
+    local_nnz: int              # this rank's block
+    row_bounds: List[int]
+    row_nnz: Optional[np.ndarray] = None  # this rank's rows' nnz(C(i,:))
+
+
+def forecast_distributed(a: Optional[CsrMatrix], b: Optional[CsrMatrix], *, same: bool = False, src: int = 0,
+                         device=None, group=None, local_forecast: Optional[Callable] = None,
+                         local_nprod: Optional[Callable] = None) -> DistributedForecast:
+    """nnz(C) of C = A*B without computing C, row-partitioned like
+    multiply_distributed. ``local_forecast(A_block, B)`` returns the block's per-row
+    nnz(C) (default: the B200 library's forecast_nnz)."""
+    import torch
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev_index = None if device is None else (device.index if hasattr(device, "index") else int(str(device).split(":")[-1]))
+    if local_forecast is None or local_nprod is None:
+        from . import api as sg
+        if local_forecast is None:
+            def local_forecast(x, y):  # noqa: E306
+                return sg.forecast_nnz(x, y, device=dev_index).row_nnz
+        if local_nprod is None:
+            def local_nprod(x, y):  # noqa: E306
+                return sg.compute_nprod(x, y, device=dev_index)[0]
+    B = broadcast_csr(b if rank == src else None, src, device, group)
+    A = B if same else broadcast_csr(a if rank == src else None, src, device, group)
+    nprod = np.asarray(local_nprod(A, B), np.int64)
+    bounds = nprod_split(nprod, world)
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    rows = np.asarray(local_forecast(slice_rows(A, r0, r1), B), np.int64) if r1 > r0 else np.zeros(0, np.int64)
+    local = int(rows.sum())
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    t = torch.tensor([local], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, group=group)
+    return DistributedForecast(int(t.item()), int(nprod.sum()), local, bounds, rows)

@@ -57,6 +57,51 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
+def _worker_forecast(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_2206_07244_b200.distributed import forecast_distributed
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = random_csr(500, 500, 0.03, 9) if rank == 0 else None
+        f = forecast_distributed(a, a, same=True,
+                                 local_forecast=lambda x, y: np.diff(np.asarray(O.spgemm(x, y).rpt)),
+                                 local_nprod=lambda x, y: O.compute_nprod(x, y)[0])
+        out = dict(rank=rank, total=f.total_nnz, local=f.local_nnz, bounds=f.row_bounds,
+                   rows=f.row_nnz.tolist(), nprod=f.total_nprod)
+        if rank == 0:
+            exp = O.spgemm(a, a)
+            out["exp_rows"] = np.diff(np.asarray(exp.rpt)).tolist()
+            out["exp_nprod"] = O.compute_nprod(a, a)[1]
+        q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_forecast():
+    """forecast_distributed: the per-rank symbolic counts add up to the single-shot C."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_forecast, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted((q.get(timeout=120) for _ in procs), key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    r0, r1 = outs
+    assert r0["bounds"] == r1["bounds"]
+    assert r0["rows"] + r1["rows"] == r0["exp_rows"]
+    assert r0["total"] == r1["total"] == sum(r0["exp_rows"]) == r0["local"] + r1["local"]
+    assert r0["nprod"] == r0["exp_nprod"]
+
+
 @pytest.mark.parametrize("case", ["square", "rect"])
 def test_two_rank_gloo_matches_single_shot(case):
     ctx = mp.get_context("spawn")
