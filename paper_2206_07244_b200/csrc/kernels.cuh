@@ -113,11 +113,6 @@ struct Spec {
 };
 
 // Claim accounting of a speculative row (shared memory, one per group).
-struct ClaimBudget {
-  int* count;     // claims so far
-  int* overflow;  // set when a claim was refused
-  int cap;
-};
 
 __device__ __forceinline__ int classify_bin(long long v, const BinUpper& up) {
   int j = 0;
@@ -145,9 +140,13 @@ __device__ __forceinline__ unsigned group_mask() {
 
 template <int G>
 __device__ __forceinline__ int group_sum(int v, unsigned gm) {
+  if constexpr (G == 32) {
+    return static_cast<int>(__reduce_add_sync(gm, static_cast<unsigned>(v)));  // one REDUX
+  } else {
 #pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o, G);
-  return v;
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o, G);
+    return v;
+  }
 }
 
 // ------------------------------------------------------------ hash tables
@@ -210,21 +209,16 @@ __device__ __forceinline__ int sym_insert(Slot* tab, int32_t key, const Hash& hs
   return sym_insert_slow(tab, key, hs, h, cur);
 }
 
+// Probing after a first-probe miss. `claims` (may be null) counts this lane's
+// new keys -- the speculative numeric's budget, summed over the group per step.
 __device__ __forceinline__ uint32_t num_slot_slow(int32_t* keys, int32_t key, const Hash& hs, uint32_t h,
-                                               int32_t cur, const ClaimBudget* bud = nullptr,
-                                               uint32_t dummy = 0) {
+                                               int32_t cur, int* claims = nullptr) {
   while (true) {
     if (cur == key) return h;
     if (cur == -1) {
-      if (bud) {  // speculative row: refuse claims past the budget (the row is abandoned)
-        if (*reinterpret_cast<volatile int*>(bud->count) >= bud->cap) {
-          *reinterpret_cast<volatile int*>(bud->overflow) = 1;
-          return dummy;
-        }
-      }
       cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, key);
       if (cur == -1) {
-        if (bud) atomicAdd(bud->count, 1);
+        if (claims) ++*claims;
         return h;
       }
       if (cur == key) return h;
@@ -262,17 +256,30 @@ __device__ __forceinline__ int sym_insert_batch(int32_t* tab, const int32_t (&ke
 // Slot of each key (claimed if new); invalid entries (key < 0) get `dummy`.
 template <int V>
 __device__ __forceinline__ void num_slot_batch(int32_t* keys, const int32_t (&key)[V], const Hash& hs,
-                                               uint32_t dummy, uint32_t (&slot)[V],
-                                               const ClaimBudget* bud = nullptr) {
+                                               uint32_t dummy, uint32_t (&slot)[V], int* claims = nullptr) {
   int32_t cur[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) slot[v] = hs.home(key[v]) & hs.mask;
 #pragma unroll
   for (int v = 0; v < V; ++v) cur[v] = key[v] >= 0 ? keys[slot[v]] : key[v];
+  // empty home slots: the V claims are issued back to back (straight-line,
+  // predicated) before any probing loop
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    if (key[v] >= 0 && cur[v] == -1) {
+      cur[v] = atomicCAS(reinterpret_cast<int*>(keys + slot[v]), -1, key[v]);
+      if (cur[v] == -1) {
+        cur[v] = key[v];
+        if (claims) ++*claims;
+      }
+    }
+  }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     if (key[v] < 0) slot[v] = dummy;
-    else if (cur[v] != key[v]) slot[v] = num_slot_slow(keys, key[v], hs, slot[v], cur[v], bud, dummy);
+    else if (cur[v] != key[v])
+      slot[v] = num_slot_slow(keys, key[v], hs, (slot[v] + 1) & hs.mask,
+                              *reinterpret_cast<volatile int32_t*>(keys + ((slot[v] + 1) & hs.mask)), claims);
   }
 }
 
@@ -716,14 +723,22 @@ __device__ __forceinline__ int walk_row(const DevCsr& A, const DevCsr& B, int64_
 // the U steps' slot lookups/claims are batched (order-independent), then the
 // U value updates run in step order with a group barrier between them; lanes
 // without a product add 0.0 into a dummy slot so the update is branch-free.
+// cap > 0 (speculative rows): the group's claims are counted per batch (a
+// register, summed with one group reduction) and the walk stops as soon as
+// they exceed cap -- returns the count (> cap: abandoned). A batch adds at most
+// U*G claims and the walk only continues while claims <= cap, so with the
+// table >= 2*cap slots (or more slots than the row has products) every claim
+// finds a free slot.
 template <int G, int U>
-__device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
-                                             int lane, unsigned gm, EntryMeta* meta, int32_t* keys,
-                                             double* vals, const Hash& hs, uint32_t dummy, int32_t* kmin_out,
-                                             int32_t* kmax_out, const ClaimBudget* bud = nullptr) {
+__device__ __forceinline__ int walk_row_num(const DevCsr& A, const DevCsr& B, int64_t a0, int64_t a1,
+                                            int lane, unsigned gm, EntryMeta* meta, int32_t* keys,
+                                            double* vals, const Hash& hs, uint32_t dummy, int32_t* kmin_out,
+                                            int32_t* kmax_out, int cap = 0) {
+  static_assert(G * U <= 128, "batch claims bounded by the speculative cap");
   // The row's column range, from the first/last column of each (sorted) B row:
   // two extra loads per A entry instead of a min/max pass over the table.
   int32_t kmin = 0x7fffffff, kmax = -1;
+  int claimed = 0;  // uniform over the group
   for (int64_t c0 = a0; c0 < a1; c0 += G) {
     const int nc = static_cast<int>(min(static_cast<int64_t>(G), a1 - c0));
     int len = 0;
@@ -742,6 +757,7 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
     __syncwarp(gm);
     if (maxlen <= G) {
       for (int j0 = 0; j0 < nc; j0 += U) {
+        if (cap && claimed > cap) break;
         int32_t kc[U];
         double x[U];
         uint32_t slot[U];
@@ -753,7 +769,8 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
           kc[u] = ok ? B.col[at] : -1;
           x[u] = ok ? __dmul_rn(m.av, B.val[at]) : 0.0;
         }
-        num_slot_batch<U>(keys, kc, hs, dummy, slot, bud);
+        int mine = 0;
+        num_slot_batch<U>(keys, kc, hs, dummy, slot, cap ? &mine : nullptr);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (j0 + u < nc) {
@@ -761,22 +778,27 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
             __syncwarp(gm);
           }
         }
+        if (cap) claimed += group_sum<G>(mine, gm);
       }
     } else {
       for (int j = 0; j < nc; ++j) {
         const EntryMeta m = meta[j];
         for (int qb = 0; qb < m.len; qb += G) {
+          if (cap && claimed > cap) break;
           const int q = qb + lane;
           int32_t kc[1] = {q < m.len ? B.col[m.b0 + q] : -1};
           const double xv = q < m.len ? __dmul_rn(m.av, B.val[m.b0 + q]) : 0.0;
           uint32_t slot[1];
-          num_slot_batch<1>(keys, kc, hs, dummy, slot, bud);
+          int mine = 0;
+          num_slot_batch<1>(keys, kc, hs, dummy, slot, cap ? &mine : nullptr);
           vals[slot[0]] = __dadd_rn(vals[slot[0]], xv);
+          if (cap) claimed += group_sum<G>(mine, gm);
         }
         __syncwarp(gm);
       }
     }
     __syncwarp(gm);
+    if (cap && claimed > cap) break;
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) {
@@ -785,6 +807,7 @@ __device__ __forceinline__ void walk_row_num(const DevCsr& A, const DevCsr& B, i
   }
   *kmin_out = kmin;
   *kmax_out = kmax;
+  return claimed;
 }
 
 // Unordered walk of ONE staged chunk (the symbolic phase has no summation
@@ -1304,7 +1327,7 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
   constexpr int LOG_T = log2_const<T>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int grp = threadIdx.x / G;
-  // per group: vals[T + 2] (slot T is the dummy), packed[NMAX], keys[T], meta[G], budget
+  // per group: vals[T + 2] (slot T is the dummy), packed[NMAX], keys[T], meta[G], 16 spare bytes
   constexpr size_t kGroupBytes = (T + 2) * 8 + NMAX * 8 + T * 4 + G * 16 + 16;
   unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * kGroupBytes;
   double* vals = reinterpret_cast<double*>(gbase);
@@ -1312,7 +1335,6 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
   uint32_t* packed32 = reinterpret_cast<uint32_t*>(packed);
   int32_t* keys = reinterpret_cast<int32_t*>(gbase + (T + 2) * 8 + NMAX * 8);
   EntryMeta* meta = reinterpret_cast<EntryMeta*>(gbase + (T + 2) * 8 + NMAX * 8 + T * 4);
-  int* budget = reinterpret_cast<int*>(gbase + (T + 2) * 8 + NMAX * 8 + T * 4 + G * 16);
   const int lane = threadIdx.x % G;
   const unsigned gm = group_mask<G>();
   const unsigned gshift = (threadIdx.x & 31u) & ~(G - 1u);
@@ -1337,15 +1359,12 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
     const Hash hs = make_hash(scale, lg);
     fill_empty<G>(keys, tsz, lane);
     fill_zero<G>(vals, tsz, lane);
-    ClaimBudget bud{budget, budget + 1, NMAX};
-    if constexpr (SPEC) {
-      if (lane == 0) budget[0] = budget[1] = 0;
-    }
     __syncwarp(gm);
     int kmin = 0x7fffffff, kmax = -1;
+    int claimed = 0;
     if constexpr (sizeof(IT) == 4) {
-      walk_row_num<G, 4>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta, keys, vals, hs,
-                         static_cast<uint32_t>(T), &kmin, &kmax, SPEC ? &bud : nullptr);
+      claimed = walk_row_num<G, 4>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta, keys, vals, hs,
+                                   static_cast<uint32_t>(T), &kmin, &kmax, SPEC ? NMAX : 0);
     } else {
       walk_row<G, 4, true, true, IT>(A, B, A.rpt[row], A.rpt[row + 1], lane, gm, meta,
                                      [keys, vals, hs](int32_t key, double x) {
@@ -1370,10 +1389,7 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
     }
     if constexpr (SPEC) {
       __syncwarp(gm);
-      const int claimed = *reinterpret_cast<volatile int*>(budget);
-      const bool over = *reinterpret_cast<volatile int*>(budget + 1) != 0 || claimed > NMAX;
-      __syncwarp(gm);
-      if (over) continue;  // abandoned (uniform): the symbolic kernel counts this row
+      if (claimed > NMAX) continue;  // abandoned (uniform): the symbolic kernel counts this row
       n = claimed;
     }
     int32_t* ocol = SPEC ? sp.col + row * sp.cap : ccol + base;
