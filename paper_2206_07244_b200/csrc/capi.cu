@@ -162,7 +162,6 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 #endif
 // 8-lane groups when B's rows average at most this many entries (else 32)
 constexpr double kG8MaxBLen = SPGEMM_G8_MAX;
-constexpr int kSpecCap = 128;                          // entries per row of the speculative scratch
 constexpr int64_t kSpecBudget = int64_t(4) << 30;      // scratch bytes the arena may spend on it
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

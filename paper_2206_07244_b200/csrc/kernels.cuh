@@ -104,6 +104,8 @@ __device__ __forceinline__ RowList RowList::resolved() const {
 // than `cap` distinct columns is abandoned (flag stays 0) and counted by the
 // symbolic kernel as usual. The symbolic walk (~1/3 of the stencil step) is
 // saved for every row that fits.
+constexpr int kSpecCap = 128;  // entries per row of the speculative scratch
+
 struct Spec {
   int32_t* col;   // [rows * cap]
   double* val;    // [rows * cap]
@@ -111,8 +113,6 @@ struct Spec {
   int cap;
   __device__ __forceinline__ bool done(int64_t row) const { return flag != nullptr && flag[row] != 0; }
 };
-
-// Claim accounting of a speculative row (shared memory, one per group).
 
 __device__ __forceinline__ int classify_bin(long long v, const BinUpper& up) {
   int j = 0;
@@ -552,66 +552,104 @@ __global__ void k_iota(int64_t* out, int64_t n) {
 // Tiles are claimed in launch order through an atomic ticket so look-back
 // always waits on tiles that are already running. A tile publishes its
 // aggregate (flag 1) and later its inclusive prefix (flag 2) in separate
-// slots, so a reader never sees one overwritten by the other.
+// slots, so a reader never sees one overwritten by the other. The look-back
+// is done by a whole warp, 32 predecessor tiles per round: it stops at the
+// nearest tile with an inclusive prefix and adds the aggregates in between.
+// Each thread's kScanItems values are moved with 16-byte accesses.
 __global__ void __launch_bounds__(kScanThreads)
     k_scan(int64_t* __restrict__ data, int64_t n, int* __restrict__ flags,
            long long* __restrict__ aggs, long long* __restrict__ incl, DevInfo* info) {
+  static_assert(kScanItems % 2 == 0, "16-byte accesses");
   __shared__ int s_tile;
   __shared__ long long s_red[32];
   __shared__ long long s_excl;
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_tile = atomicAdd(&info->tile_counter, 1);
   __syncthreads();
   const int tile = s_tile;
   const int64_t base = static_cast<int64_t>(tile) * kScanTile + threadIdx.x * kScanItems;
   long long v[kScanItems];
   long long tsum = 0;
+  const bool full = base + kScanItems <= n;
+  if (full) {
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    v[i] = (base + i < n) ? data[base + i] : 0;
-    tsum += v[i];
+    for (int i = 0; i < kScanItems; i += 2) {
+      const longlong2 x = *reinterpret_cast<const longlong2*>(data + base + i);
+      v[i] = x.x;
+      v[i + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < n) ? data[base + i] : 0;
   }
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) tsum += v[i];
   long long agg;
   const long long texcl = block_exclusive_scan<kScanThreads>(tsum, s_red, &agg);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     long long excl = 0;
     if (tile == 0) {
-      incl[0] = agg;
-      __threadfence();
-      atomicExch(&flags[0], 2);
+      if (lane == 0) {
+        incl[0] = agg;
+        __threadfence();
+        atomicExch(&flags[0], 2);
+      }
     } else {
-      aggs[tile] = agg;
-      __threadfence();
-      atomicExch(&flags[tile], 1);
-      int p = tile - 1;
+      if (lane == 0) {
+        aggs[tile] = agg;
+        __threadfence();
+        atomicExch(&flags[tile], 1);
+      }
+      int p = tile - 1;  // lane l looks at tile p - l
       while (true) {
+        const int q = p - lane;
         int f;
         do {
-          f = *reinterpret_cast<volatile int*>(&flags[p]);
-        } while (f == 0);
+          f = q >= 0 ? *reinterpret_cast<volatile int*>(&flags[q]) : 2;
+        } while (__any_sync(kFull, f == 0));
         __threadfence();
-        if (f == 2) {
-          excl += *reinterpret_cast<volatile long long*>(&incl[p]);
+        long long val = 0;
+        if (q >= 0) val = f == 2 ? *reinterpret_cast<volatile long long*>(&incl[q])
+                                 : *reinterpret_cast<volatile long long*>(&aggs[q]);
+        const unsigned m2 = __ballot_sync(kFull, f == 2);
+        if (m2) {
+          const int first = __ffs(m2) - 1;  // nearest tile holding an inclusive prefix
+          excl += warp_sum(lane <= first ? val : 0ll);
           break;
         }
-        excl += *reinterpret_cast<volatile long long*>(&aggs[p]);
-        --p;
+        excl += warp_sum(val);
+        p -= 32;
       }
-      incl[tile] = excl + agg;
-      __threadfence();
-      atomicExch(&flags[tile], 2);
+      if (lane == 0) {
+        incl[tile] = excl + agg;
+        __threadfence();
+        atomicExch(&flags[tile], 2);
+      }
     }
-    s_excl = excl;
-    if ((static_cast<int64_t>(tile) + 1) * kScanTile >= n) {
-      info->scan_total = excl + agg;
-      if (static_cast<unsigned long long>(excl + agg) != info->total) atomicOr(&info->error, kErrScanMismatch);
+    if (lane == 0) {
+      s_excl = excl;
+      if ((static_cast<int64_t>(tile) + 1) * kScanTile >= n) {
+        info->scan_total = excl + agg;
+        if (static_cast<unsigned long long>(excl + agg) != info->total) atomicOr(&info->error, kErrScanMismatch);
+      }
     }
   }
   __syncthreads();
   long long run = s_excl + texcl;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    if (base + i < n) data[base + i] = run;
-    run += v[i];
+    const long long x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  if (full) {
+#pragma unroll
+    for (int i = 0; i < kScanItems; i += 2)
+      *reinterpret_cast<longlong2*>(data + base + i) = make_longlong2(v[i], v[i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+      if (base + i < n) data[base + i] = v[i];
   }
 }
 
@@ -1655,12 +1693,17 @@ __global__ void __launch_bounds__(kGlobalThreads)
 
 // Numeric phase, first launch: the rows finished speculatively in the symbolic
 // phase are copied from the scratch into C. A warp takes 32 consecutive rows:
-// flags and row pointers load coalesced, then the lanes copy row by row.
+// flags and row pointers load coalesced, then the lanes copy two rows at a
+// time with every load of both rows (<= kSpecCap entries each) issued before
+// the first store -- 16 independent loads per lane in flight.
 __global__ void __launch_bounds__(256)
     k_spec_copy(Spec sp, const int64_t* __restrict__ rpt, int64_t M, int32_t* __restrict__ ccol,
                 double* __restrict__ cval) {
+  constexpr int kIt = kSpecCap / 32;
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int32_t* __restrict__ scol = sp.col;
+  const double* __restrict__ sval = sp.val;
   for (int64_t r0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; r0 < M;
        r0 += warps * 32) {
     const int64_t r = r0 + lane;
@@ -1669,15 +1712,37 @@ __global__ void __launch_bounds__(256)
     const int n = mine ? static_cast<int>(rpt[r + 1] - base) : 0;
     unsigned todo = __ballot_sync(kFull, mine && n > 0);
     while (todo) {
-      const int l = __ffs(todo) - 1;
-      todo &= todo - 1u;
-      const int64_t b = __shfl_sync(kFull, base, l);
-      const int nn = __shfl_sync(kFull, n, l);
-      const int64_t s0 = (r0 + l) * sp.cap;
-      for (int e = lane; e < nn; e += 32) {
-        ccol[b + e] = sp.col[s0 + e];
-        cval[b + e] = sp.val[s0 + e];
+      int64_t b[2], s0[2];
+      int nn[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int l = todo ? __ffs(todo) - 1 : 0;
+        const bool have = todo != 0;
+        todo &= todo - 1u;
+        b[k] = __shfl_sync(kFull, base, l);
+        nn[k] = have ? __shfl_sync(kFull, n, l) : 0;
+        s0[k] = (r0 + l) * kSpecCap;
       }
+      int32_t c[2][kIt];
+      double v[2][kIt];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int i = 0; i < kIt; ++i) {
+          const int e = lane + 32 * i;
+          c[k][i] = e < nn[k] ? scol[s0[k] + e] : 0;
+          v[k][i] = e < nn[k] ? sval[s0[k] + e] : 0.0;
+        }
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int i = 0; i < kIt; ++i) {
+          const int e = lane + 32 * i;
+          if (e < nn[k]) {
+            ccol[b[k] + e] = c[k][i];
+            cval[b[k] + e] = v[k][i];
+          }
+        }
     }
   }
 }
