@@ -1117,13 +1117,19 @@ __global__ void __launch_bounds__(128)
       vals[s * 32] = 0.0;
     }
     const int64_t a1 = A.rpt[row + 1];
-    for (int64_t p = A.rpt[row]; p < a1; ++p) {
-      const int32_t k = A.col[p];
-      const double av = A.val[p];
-      const int64_t b1 = B.rpt[k + 1];
-      for (int64_t q = B.rpt[k]; q < b1; ++q) {
-        const int32_t key = B.col[q];
-        const double x = __dmul_rn(av, B.val[q]);
+    // A entries two at a time: both B row ranges, then up to QB entries of each
+    // B row, are loaded before any is inserted (independent loads in flight
+    // instead of one dependent chain per product)
+    constexpr int QB = 8;
+    for (int64_t p = A.rpt[row]; p < a1; p += 2) {
+      const bool two = p + 1 < a1;
+      const int32_t k0 = A.col[p];
+      const int32_t k1 = two ? A.col[p + 1] : k0;
+      const double av0 = A.val[p];
+      const double av1 = two ? A.val[p + 1] : 0.0;
+      const int64_t q0 = B.rpt[k0], e0 = B.rpt[k0 + 1];
+      const int64_t q1 = B.rpt[k1], e1 = two ? B.rpt[k1 + 1] : q1;
+      auto insert = [&](int32_t key, double x) {
         uint32_t h = hs.home(key);
         while (true) {
           const int32_t c = keys[h * 32];
@@ -1135,20 +1141,76 @@ __global__ void __launch_bounds__(128)
           h = (h + 1) & (TS - 1);
         }
         vals[h * 32] = __dadd_rn(vals[h * 32], x);
+      };
+      int32_t c0[QB], c1[QB];
+      double v0[QB], v1[QB];
+#pragma unroll
+      for (int i = 0; i < QB; ++i) {
+        c0[i] = q0 + i < e0 ? B.col[q0 + i] : -1;
+        v0[i] = q0 + i < e0 ? B.val[q0 + i] : 0.0;
       }
+#pragma unroll
+      for (int i = 0; i < QB; ++i) {
+        c1[i] = q1 + i < e1 ? B.col[q1 + i] : -1;
+        v1[i] = q1 + i < e1 ? B.val[q1 + i] : 0.0;
+      }
+      // entry p (its whole B row) strictly before entry p + 1: the reference's order
+#pragma unroll
+      for (int i = 0; i < QB; ++i)
+        if (c0[i] >= 0) insert(c0[i], __dmul_rn(av0, v0[i]));
+      for (int64_t q = q0 + QB; q < e0; ++q) insert(B.col[q], __dmul_rn(av0, B.val[q]));
+#pragma unroll
+      for (int i = 0; i < QB; ++i)
+        if (c1[i] >= 0) insert(c1[i], __dmul_rn(av1, v1[i]));
+      for (int64_t q = q1 + QB; q < e1; ++q) insert(B.col[q], __dmul_rn(av1, B.val[q]));
     }
     // compact in place: entry m <- slot s (m <= s), keys and values together
     int m = 0;
+    int32_t kmin = 0x7fffffff, kmax = -1;
 #pragma unroll
     for (int s = 0; s < TS; ++s) {
       const int32_t c = keys[s * 32];
       if (c != -1) {
         keys[m * 32] = c;
         vals[m * 32] = vals[s * 32];
+        kmin = min(kmin, c);
+        kmax = max(kmax, c);
         ++m;
       }
     }
     if (m != n) atomicOr(&info->error, kErrNumericCount);
+    constexpr int LG = log2_const<NMAX>();
+    if (static_cast<uint32_t>(kmax - kmin) < (0xffffffffu >> LG)) {
+      // narrow row: 32-bit keys (col - kmin) << LG | entry, sorted with min/max pairs
+      uint32_t v[NMAX];
+#pragma unroll
+      for (int i = 0; i < NMAX; ++i)
+        v[i] = i < m ? (static_cast<uint32_t>(keys[i * 32] - kmin) << LG) | static_cast<uint32_t>(i) : 0xffffffffu;
+#pragma unroll
+      for (int k = 2; k <= NMAX; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+          for (int i = 0; i < NMAX; ++i) {
+            const int pi = i ^ j;
+            if (pi > i) {
+              const uint32_t a = v[i], b = v[pi];
+              const bool up = (i & k) == 0;
+              v[i] = up ? min(a, b) : max(a, b);
+              v[pi] = up ? max(a, b) : min(a, b);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NMAX; ++i) {
+        if (i < m) {
+          ccol[base + i] = kmin + static_cast<int32_t>(v[i] >> LG);
+          cval[base + i] = vals[(v[i] & (NMAX - 1u)) * 32];
+        }
+      }
+      continue;
+    }
     unsigned long long v[NMAX];
 #pragma unroll
     for (int i = 0; i < NMAX; ++i)
