@@ -454,46 +454,110 @@ __global__ void __launch_bounds__(kBinThreads)
 
 // K3a: bin sizes, bin offsets (exclusive sum over bins, binning.cpp:304-305),
 // fast-path flag, and the per-row-block write cursors in row-block order
-// (the deterministic reservation of binning.cpp:220-229). One block.
+// (the deterministic reservation of binning.cpp:220-229). One block; thread t
+// holds row block t's 8 bin counts (one 32-byte load) and the 8 bins are
+// scanned together -- per bin one warp-shuffle scan over the lanes and one
+// over the 32 warp totals, three barriers per 1024 row blocks.
 __global__ void __launch_bounds__(1024)
     k_bin_offsets(int32_t* __restrict__ blk_counts, int64_t nrb, int64_t M, long long upper0,
                   DevInfo* info) {
-  __shared__ long long s_red[32];
-  __shared__ long long s_bin[kNumBins];
-  long long local[kNumBins];
+  static_assert(kNumBins == 8, "one int4 pair per row block");
+  __shared__ int s_warp[32][kNumBins];
+  __shared__ int s_wpre[32][kNumBins];
+  __shared__ int s_tile[kNumBins];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool single = nrb <= 1024;  // one tile: totals and cursors from one scan
+  long long carry[kNumBins];         // per bin: counts of the earlier tiles
+  long long off[kNumBins];           // per bin: segment start (exclusive sum over bins)
 #pragma unroll
-  for (int j = 0; j < kNumBins; ++j) local[j] = 0;
-  for (int64_t b = threadIdx.x; b < nrb; b += 1024) {
-#pragma unroll
-    for (int j = 0; j < kNumBins; ++j) local[j] += blk_counts[b * kNumBins + j];
-  }
-#pragma unroll 1
-  for (int j = 0; j < kNumBins; ++j) {
-    const long long t = block_sum_ll<1024>(local[j], s_red);
-    if (threadIdx.x == 0) s_bin[j] = t;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    long long run = 0;
-    for (int j = 0; j < kNumBins; ++j) {
-      info->bin_size[j] = s_bin[j];
-      info->bin_offset[j] = run;
-      run += s_bin[j];
-    }
-    info->fast_path = (M == 0 || info->max_metric <= upper0) ? 1 : 0;
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int j = 0; j < kNumBins; ++j) {
-    long long carry = 0;
-    for (int j2 = 0; j2 < j; ++j2) carry += s_bin[j2];
+  for (int j = 0; j < kNumBins; ++j) carry[j] = off[j] = 0;
+  // pass 0: per-bin totals (sizes, offsets); pass 1 (several tiles only): cursors
+  for (int pass = 0; pass < (single ? 1 : 2); ++pass) {
     for (int64_t t0 = 0; t0 < nrb; t0 += 1024) {
       const int64_t b = t0 + threadIdx.x;
-      const long long v = b < nrb ? blk_counts[b * kNumBins + j] : 0;
-      long long tile_total;
-      const long long ex = block_exclusive_scan<1024>(v, s_red, &tile_total);
-      if (b < nrb) blk_counts[b * kNumBins + j] = static_cast<int32_t>(carry + ex);
-      carry += tile_total;
+      int v[kNumBins];
+      if (b < nrb) {
+        const int4* src = reinterpret_cast<const int4*>(blk_counts + b * kNumBins);
+        const int4 x = src[0], y = src[1];
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kNumBins; ++j) v[j] = 0;
+      }
+      int inc[kNumBins];  // inclusive within the warp (a tile holds < 2^31 rows)
+#pragma unroll
+      for (int j = 0; j < kNumBins; ++j) {
+        int x = v[j];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        inc[j] = x;
+      }
+      if (lane == 31) {
+#pragma unroll
+        for (int j = 0; j < kNumBins; ++j) s_warp[warp][j] = inc[j];
+      }
+      __syncthreads();
+      if (warp < kNumBins) {  // warp j scans bin j's 32 warp totals
+        const int j = warp;
+        const int x0 = s_warp[lane][j];
+        int x = x0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        s_wpre[lane][j] = x - x0;
+        if (lane == 31) s_tile[j] = x;
+      }
+      __syncthreads();
+      long long before[kNumBins], tile[kNumBins];
+#pragma unroll
+      for (int j = 0; j < kNumBins; ++j) {
+        before[j] = s_wpre[warp][j];
+        tile[j] = s_tile[j];
+      }
+      if (single) {
+        long long run = 0;
+#pragma unroll
+        for (int j = 0; j < kNumBins; ++j) {
+          off[j] = run;
+          run += tile[j];
+        }
+      }
+      if ((single || pass == 1) && b < nrb) {
+        int cur[kNumBins];
+#pragma unroll
+        for (int j = 0; j < kNumBins; ++j)
+          cur[j] = static_cast<int32_t>(off[j] + carry[j] + before[j] + inc[j] - v[j]);
+        int4* dst = reinterpret_cast<int4*>(blk_counts + b * kNumBins);
+        dst[0] = make_int4(cur[0], cur[1], cur[2], cur[3]);
+        dst[1] = make_int4(cur[4], cur[5], cur[6], cur[7]);
+      }
+#pragma unroll
+      for (int j = 0; j < kNumBins; ++j) carry[j] += tile[j];
+      __syncthreads();  // s_warp is reused by the next tile
+    }
+    if (pass == 0) {
+      long long run = 0;
+#pragma unroll
+      for (int j = 0; j < kNumBins; ++j) {
+        off[j] = run;
+        run += carry[j];
+      }
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < kNumBins; ++j) {
+          info->bin_size[j] = carry[j];
+          info->bin_offset[j] = off[j];
+        }
+        info->fast_path = (M == 0 || info->max_metric <= upper0) ? 1 : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < kNumBins; ++j) carry[j] = 0;
     }
   }
 }
