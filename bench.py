@@ -610,7 +610,9 @@ def run_config5(args):
 def run_e2e(sg, torch, a_host, min_steps, device):
     """Same metric through the public API with host buffers: each step copies A from
     pinned host memory (B aliases A), multiplies, and reads C back into pinned host
-    buffers -- one synchronous call per step (`value`). Reported alongside: the
+    buffers -- one synchronous `multiply_into` call per step (`value`; inside it, row
+    blocks' C downloads overlap the next blocks' kernels). Reported alongside: the same
+    as separate calls (`separate_calls_value`: run_device, then download_into) and the
     pipelined mode of an application issuing independent products back to back
     (`pipelined_value`: step i's C download via DeviceMatrix.download_async on the
     context's copy lane overlaps step i+1's upload and kernels, at most two
@@ -643,6 +645,11 @@ def run_e2e(sg, torch, a_host, min_steps, device):
         issued[0] += 1
         if issued[0] % 2 == 0:  # double buffering: at most two products in flight
             ctx.wait_downloads()
+        return out.stats.total_nprod
+
+    def step_into():
+        n, out = sg.multiply_into(a, a, orpt.numpy(), ocol.numpy(), oval.numpy(), device=device,
+                                  parts=int(os.environ.get("SPGEMM_INTO_PARTS", 0)))
         return out.stats.total_nprod
 
     def step_sync():
@@ -688,10 +695,14 @@ def run_e2e(sg, torch, a_host, min_steps, device):
         gc.enable()
         return nprod, time.perf_counter() - t0, steps
 
-    nprod_p, t_p, steps = timed(step_pipelined, None)
-    nprod, t, _ = timed(step_sync, steps)
+    nprod, t, steps = timed(step_into, None)
+    nprod_s, t_s, _ = timed(step_sync, steps)
+    nprod_p, t_p, _ = timed(step_pipelined, steps)
     return {"value": 2 * nprod / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": steps, "ms_per_step": t / steps * 1e3, "mode": "one synchronous call per step",
+            "steps": steps, "ms_per_step": t / steps * 1e3,
+            "mode": "one synchronous multiply_into call per step (host A in, host C out; row blocks' C "
+                    "downloads overlap the next blocks' kernels)",
+            "separate_calls_value": 2 * nprod_s / t_s / 1e9, "separate_calls_ms_per_step": t_s / steps * 1e3,
             "pipelined_value": 2 * nprod_p / t_p / 1e9, "pipelined_ms_per_step": t_p / steps * 1e3}
 
 

@@ -226,6 +226,21 @@ spgemm_status spgemm_multiply_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_c
 spgemm_status spgemm_matrices_download_stitched(spgemm_ctx** ctxs, spgemm_matrix* const* slices, int32_t n,
                                                 int64_t* rpt, int32_t* col, double* val);
 
+/* ------------------------------------------- host in, host out, overlapped */
+/* B200 extension: C = A*B from host operands into caller-provided host buffers
+ * (rpt: a->rows + 1 entries; col/val: capacity entries -- size them with
+ * spgemm_forecast_nnz or a previous product; pinned memory gives full PCIe
+ * bandwidth). A and B are staged once; A's rows are split into `parts` blocks
+ * by the nprod prefix sum (parts <= 0: chosen from the product's size), and
+ * each block's C is downloaded on the copy lane while the next block is
+ * multiplied, so the device->host transfer of C overlaps the kernels instead of
+ * following them. Values and structure are those of spgemm_multiply (rows are
+ * independent). *nnz receives nnz(C); SPGEMM_INVALID_ARGUMENT when C exceeds
+ * the capacity (nothing past it is written). */
+spgemm_status spgemm_multiply_into(spgemm_ctx* ctx, const spgemm_csr_view* a, const spgemm_csr_view* b,
+                                   const spgemm_options* opts, int32_t parts, int64_t* rpt, int64_t capacity,
+                                   int32_t* col, double* val, int64_t* nnz, spgemm_report* report);
+
 /* ------------------------------------------------ symbolic-only sizing */
 /* B200 extension: nnz(C) without computing or
  * allocating C -- the reference's step API run as setup + symbolic_binning +

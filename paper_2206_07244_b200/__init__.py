@@ -10,5 +10,5 @@ from .api import (  # noqa: F401
     forecast_nnz_multi, get_context,
     kDefaultNumPreset, kDefaultSymPreset, kMaxSymbolicTableSize, kNoUpperBound, kNumBins,
     kSymbolicSpillThreshold, make_execution_plan, max_relative_error, multiply, multiply_device,
-    multiply_multi, numeric_preset, preset, preset_names, run_binning, same_pattern, symbolic_preset, validate_csr,
+    multiply_into, multiply_multi, numeric_preset, preset, preset_names, run_binning, same_pattern, symbolic_preset, validate_csr,
 )

@@ -128,6 +128,8 @@ _decl("spgemm_ctx_wait_downloads", _st, [_P])
 _decl("spgemm_multiply_multi", _st, [_P, C.c_int32, _P, _P, _P, _P, _P, _P])
 _decl("spgemm_matrices_download_stitched", _st, [_P, _P, C.c_int32, _P, _P, _P])
 _decl("spgemm_compute_nprod", _st, [_P, C.POINTER(CsrView), C.POINTER(CsrView), _P, C.POINTER(C.c_int64)])
+_decl("spgemm_multiply_into", _st, [_P, C.POINTER(CsrView), C.POINTER(CsrView), _P, C.c_int32, _P, C.c_int64,
+                                    _P, _P, C.POINTER(C.c_int64), C.POINTER(Report)])
 _decl("spgemm_forecast_nnz", _st, [_P, C.POINTER(CsrView), C.POINTER(CsrView), _P, _P, C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int64)])
 _decl("spgemm_forecast_nnz_multi", _st, [_P, C.c_int32, C.POINTER(CsrView), C.POINTER(CsrView), _P, _P, _P,
@@ -148,6 +150,7 @@ EXPORTED = [
     "spgemm_matrix_device_ptrs", "spgemm_matrix_download", "spgemm_matrix_free", "spgemm_matrix_checksum",
     "spgemm_matrix_download_async", "spgemm_ctx_wait_downloads", "spgemm_multiply_multi",
     "spgemm_matrices_download_stitched", "spgemm_compute_nprod", "spgemm_forecast_nnz", "spgemm_forecast_nnz_multi",
+    "spgemm_multiply_into",
     "spgemm_build_rpt", "spgemm_run_binning",
 ]
 

@@ -756,6 +756,33 @@ def multiply_multi(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] 
     return out
 
 
+def multiply_into(a: CsrMatrix, b: CsrMatrix, rpt: np.ndarray, col: np.ndarray, val: np.ndarray,
+                  options: Optional[SpgemmOptions] = None, device: Optional[int] = None, parts: int = 0):
+    """C = A*B from host operands into caller buffers (C ABI spgemm_multiply_into):
+    rpt int64[a.rows + 1], col int32 / val float64 of capacity >= nnz(C) (size them with
+    forecast_nnz or a previous product; pinned buffers run at full PCIe speed). A's rows
+    go in `parts` nprod-balanced blocks (0: by size) and each block's C is downloaded
+    while the next block is multiplied. Returns (nnz, SpgemmOutput without c)."""
+    if a.on_device or b.on_device:
+        raise InvalidArgument("multiply_into: operands must be host-resident")
+    if rpt.dtype != np.int64 or col.dtype != np.int32 or val.dtype != np.float64:
+        raise InvalidArgument("multiply_into: rpt int64, col int32, val float64")
+    if rpt.size < a.rows + 1 or not (rpt.flags.c_contiguous and col.flags.c_contiguous and val.flags.c_contiguous):
+        raise InvalidArgument("multiply_into: rpt needs a.rows + 1 entries; contiguous buffers")
+    cap = min(col.size, val.size)
+    va, vb = a._view(), b._view()
+    if a is not b and a.rpt is b.rpt:
+        vb = va
+    nnz = C.c_int64()
+    rep = _c.Report()
+    opts = options._c() if options is not None else None
+    _check(_c.lib.spgemm_multiply_into(get_context(device).handle, C.byref(va), C.byref(vb),
+                                       C.byref(opts) if opts is not None else None, int(parts), rpt.ctypes.data,
+                                       cap, col.ctypes.data if cap else None, val.ctypes.data if cap else None,
+                                       C.byref(nnz), C.byref(rep)))
+    return int(nnz.value), _output_from(rep, None, options)
+
+
 @dataclass
 class NnzForecast:
     """Symbolic-only sizing of C = A*B."""

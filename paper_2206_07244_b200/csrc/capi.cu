@@ -36,6 +36,11 @@ using namespace spgemm_b200;
 namespace {
 
 thread_local std::string g_err;
+// set while multiply_into runs its row blocks: their device operands were
+// staged on the context's own stream, so no ordering against the legacy
+// default stream is needed (that wait would also order the blocks behind
+// unrelated blocking-stream work)
+thread_local bool g_inputs_stream_ordered = false;
 
 struct Err {
   spgemm_status s;
@@ -176,7 +181,10 @@ struct spgemm_ctx {
   cudaStream_t bin_s[kNumBins] = {};
   cudaEvent_t ev_fork = nullptr, ev_side = nullptr, ev_info = nullptr;
   cudaEvent_t ev_join[kNumBins] = {};
-  DevInfo* h_info = nullptr;  // pinned, two slots
+  DevInfo* h_info = nullptr;      // pinned and mapped, two slots
+  DevInfo* h_info_dev = nullptr;  // h_info's device address (written by k_info_to_host)
+  int64_t* h_scalar = nullptr;    // pinned and mapped scalar (k_read_i64)
+  int64_t* h_scalar_dev = nullptr;
   std::atomic<int64_t> launches{0};
   std::mutex attr_mu;
   std::unordered_set<const void*> attr_done;
@@ -403,9 +411,12 @@ struct spgemm_pipeline {
     ck(cudaEventElapsedTime(&ms, ev[i], ev[j]), "cudaEventElapsedTime");
     return ms * 1e-3;
   }
+  // DevInfo -> pinned host slot `slot` (k_info_to_host, no copy engine), stream-ordered
+  void info_to_host(const DevInfo* d, int slot, int count, cudaStream_t s) {
+    SPG_LAUNCH(ctx, "k_info_to_host", s, k_info_to_host<<<1, 64, 0, s>>>(d, ctx->h_info_dev + slot, count));
+  }
   void fetch_info(DevInfo* d, DevInfo* h) {
-    ck(cudaMemcpyAsync(ctx->h_info, d, sizeof(DevInfo), cudaMemcpyDeviceToHost, ctx->main_s),
-       "D2H info");
+    info_to_host(d, 0, 1, ctx->main_s);
     ck(cudaStreamSynchronize(ctx->main_s), "cudaStreamSynchronize");
     *h = *ctx->h_info;
   }
@@ -439,7 +450,20 @@ void stage_input(spgemm_ctx* ctx, const spgemm_csr_view* v, DevCsr* d, void** ow
     fail(SPGEMM_INVALID_ARGUMENT, "row count exceeds the 32-bit row-id range");
   if (!v->rpt) fail(SPGEMM_INVALID_ARGUMENT, "null rpt");
   if (v->on_device) {
-    ck(cudaMemcpy(nnz, v->rpt + v->rows, sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H nnz");
+    // Device operands written by work on the legacy default stream (a torch
+    // copy, say) are ordered before this product's kernels.
+    if (!g_inputs_stream_ordered) {
+      cudaEvent_t e = pooled_event(ctx);
+      ck(cudaEventRecord(e, cudaStreamLegacy), "record default stream");
+      ck(cudaStreamWaitEvent(ctx->main_s, e, 0), "main waits for default stream");
+      ctx->ev_pool.push_back(e);
+    }
+    // nnz = rpt[rows], read by an SM into mapped host memory (a copy-engine
+    // read-back would queue behind downloads in flight on the copy lane)
+    SPG_LAUNCH(ctx, "k_read_i64", ctx->main_s,
+               k_read_i64<<<1, 1, 0, ctx->main_s>>>(v->rpt + v->rows, ctx->h_scalar_dev));
+    ck(cudaStreamSynchronize(ctx->main_s), "cudaStreamSynchronize");
+    *nnz = *const_cast<volatile int64_t*>(ctx->h_scalar);
     d->rpt = v->rpt;
     d->col = v->col;
     d->val = v->val;
@@ -702,8 +726,7 @@ void spgemm_pipeline::numeric_binning() {
   }
   // The pass-1 total sizes C; read it back while the scatter runs and start
   // the C allocation on the side lane (pipeline.cpp:245-257).
-  ck(cudaMemcpyAsync(ctx->h_info + 1, d_info_num, sizeof(DevInfo), cudaMemcpyDeviceToHost, s),
-     "D2H num info");
+  info_to_host(d_info_num, 1, 1, s);
   ck(cudaEventRecord(ctx->ev_info, s), "ev_info");
   if (M > 0) {
     SPG_LAUNCH(ctx, "k_bin_scatter", s,
@@ -859,8 +882,7 @@ void spgemm_pipeline::run_numeric() {
 
 void spgemm_pipeline::finish(spgemm_report* r) {
   expect(kNumeric, "finish");
-  ck(cudaMemcpyAsync(ctx->h_info, d_info_sym, 2 * sizeof(DevInfo), cudaMemcpyDeviceToHost, ctx->main_s),
-     "D2H infos");
+  info_to_host(d_info_sym, 0, 2, ctx->main_s);
   ck(cudaStreamSynchronize(ctx->main_s), "cudaStreamSynchronize");
   const DevInfo sym = ctx->h_info[0], num = ctx->h_info[1];
   if (num.error & kErrScanMismatch)
@@ -970,13 +992,23 @@ spgemm_status spgemm_ctx_create(int32_t device, spgemm_ctx** out) {
       ck(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming), "event");
       ck(cudaEventCreateWithFlags(&c->ev_info, cudaEventDisableTiming), "event");
       for (auto& e : c->ev_join) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-      ck(cudaMallocHost(&c->h_info, 2 * sizeof(DevInfo)), "cudaMallocHost");
+      ck(cudaHostAlloc(&c->h_info, 2 * sizeof(DevInfo), cudaHostAllocMapped | cudaHostAllocPortable),
+         "cudaHostAlloc");
+      ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_info_dev), c->h_info, 0), "cudaHostGetDevicePointer");
+      ck(cudaHostAlloc(&c->h_scalar, 64, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
+      ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_scalar_dev), c->h_scalar, 0),
+         "cudaHostGetDevicePointer");
       // Keep freed blocks in the stream-ordered pool: repeated multiplies
       // reuse HBM without returning it to the driver.
       cudaMemPool_t pool;
       ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
       uint64_t thresh = std::numeric_limits<uint64_t>::max();
       ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh), "pool attr");
+      // Never make an allocation wait on another stream's free: C freed on the
+      // copy lane behind its download must not stall the next product's
+      // kernels (the pool takes fresh memory instead).
+      int no = 0;
+      ck(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no), "pool attr");
     } catch (...) {
       spgemm_ctx_destroy(c);
       throw;
@@ -1007,6 +1039,7 @@ void spgemm_ctx_destroy(spgemm_ctx* c) {
   for (auto& e : c->ev_pool) cudaEventDestroy(e);
   for (auto& b : c->scratch) cudaFree(b.p);
   if (c->h_info) cudaFreeHost(c->h_info);
+  if (c->h_scalar) cudaFreeHost(c->h_scalar);
   if (prev >= 0) cudaSetDevice(prev);
   delete c;
 }
@@ -1396,6 +1429,137 @@ spgemm_status spgemm_compute_nprod(spgemm_ctx* ctx, const spgemm_csr_view* a,
   std::string keep = g_err;
   spgemm_pipeline_destroy(p);
   g_err = keep;
+  return st;
+}
+
+spgemm_status spgemm_multiply_into(spgemm_ctx* ctx, const spgemm_csr_view* a, const spgemm_csr_view* b,
+                                   const spgemm_options* opts, int32_t parts, int64_t* rpt, int64_t capacity,
+                                   int32_t* col, double* val, int64_t* nnz_out, spgemm_report* report) {
+  std::vector<void*> staged;
+  std::vector<spgemm_matrix*> pending;
+  auto cleanup = [&] {
+    for (spgemm_matrix* m : pending) spgemm_matrix_free(m);
+    cudaStreamSynchronize(ctx->side_s);
+    for (void* p : staged) scratch_release(ctx, p);
+  };
+  const spgemm_status st = guard([&] {
+    DeviceGuard g(ctx->device);
+    if (!a || !b || !rpt || (capacity > 0 && (!col || !val)))
+      fail(SPGEMM_INVALID_ARGUMENT, "spgemm_multiply_into: null argument");
+    if (a->on_device || b->on_device)
+      fail(SPGEMM_INVALID_ARGUMENT, "spgemm_multiply_into: operands must be host-resident");
+    if (a->cols != b->rows)
+      fail(SPGEMM_INVALID_ARGUMENT, "spgemm: a.cols (" + std::to_string(a->cols) + ") != b.rows (" +
+                                        std::to_string(b->rows) + ")");
+    // 1. stage A and B once (B aliasing A is staged once)
+    DevCsr da{}, db{};
+    void* own[3] = {nullptr, nullptr, nullptr};
+    int64_t a_nnz = 0, b_nnz = 0;
+    stage_input(ctx, a, &da, own, &a_nnz);
+    staged.insert(staged.end(), own, own + 3);
+    const bool alias = a->rpt == b->rpt && a->col == b->col && a->val == b->val && a->rows == b->rows;
+    if (alias) {
+      db = da;
+      b_nnz = a_nnz;
+    } else {
+      void* ownb[3] = {nullptr, nullptr, nullptr};
+      stage_input(ctx, b, &db, ownb, &b_nnz);
+      staged.insert(staged.end(), ownb, ownb + 3);
+    }
+    const spgemm_csr_view vb{b->rows, b->cols, db.rpt, db.col, db.val, 1};
+    // 2. the block split: equal shares of A's nonzeros, from the host row
+    // pointers (no device round trip); the block count from the estimated size
+    // of C (nnz(A) x mean B row length products)
+    const int64_t M = a->rows;
+    if (parts <= 0) {  // ~1.5 GB of (upper-bound) C per block, at most 8 blocks
+      const double est = static_cast<double>(a_nnz) * (b->rows > 0 ? static_cast<double>(b_nnz) / b->rows : 0.0) * 12.0;
+      parts = static_cast<int32_t>(std::min(8.0, std::max(1.0, est / (1536.0 * (1 << 20)))));
+    }
+    parts = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(parts, std::max<int64_t>(M, 1))));
+    std::vector<int64_t> bounds(static_cast<size_t>(parts) + 1, 0);
+    for (int32_t g2 = 1; g2 < parts; ++g2) {
+      const int64_t target = static_cast<int64_t>((static_cast<__int128>(a_nnz) * g2) / parts);
+      const int64_t* it = std::lower_bound(a->rpt, a->rpt + M + 1, target);
+      bounds[static_cast<size_t>(g2)] =
+          std::max(bounds[static_cast<size_t>(g2) - 1], std::min<int64_t>(M, static_cast<int64_t>(it - a->rpt)));
+    }
+    bounds[static_cast<size_t>(parts)] = M;
+    // 3. blocks in order; block i's download overlaps block i+1's kernels
+    const bool dbg = std::getenv("SPGEMM_INTO_DEBUG") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto ms_since = [&] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    };
+    int64_t* brpt = static_cast<int64_t*>(scratch_acquire(ctx, static_cast<size_t>(M + 1) * 8, ctx->main_s));
+    staged.push_back(brpt);
+    int64_t off = 0;
+    spgemm_report combined{};
+    bool first = true;
+    for (int32_t i = 0; i < parts; ++i) {
+      const int64_t r0 = bounds[static_cast<size_t>(i)], r1 = bounds[static_cast<size_t>(i) + 1];
+      if (r1 == r0 && !(M == 0 && i == 0)) continue;
+      // the block's row pointers, rebased to start at 0
+      const int64_t p0 = a->rpt[r0];
+      if (r1 > r0 || M == 0) {
+        const int64_t n = r1 - r0 + 1;
+        const int grid = static_cast<int>(std::min<int64_t>(ctx->num_sms * 4, ceil_div(n, 256)));
+        k_add_offset<<<std::max(grid, 1), 256, 0, ctx->main_s>>>(brpt + r0, da.rpt + r0, n, -p0);
+        ck(cudaGetLastError(), "k_add_offset");
+        ctx->launches.fetch_add(1);
+      }
+      const spgemm_csr_view blk{r1 - r0, a->cols, brpt + r0, da.col ? da.col + p0 : nullptr,
+                                da.val ? da.val + p0 : nullptr, 1};
+      spgemm_matrix* m = nullptr;
+      spgemm_report rep{};
+      g_inputs_stream_ordered = true;
+      const spgemm_status s2 = spgemm_multiply(ctx, &blk, &vb, opts, &m, &rep);
+      g_inputs_stream_ordered = false;
+      if (s2 != SPGEMM_OK) fail(s2, g_err);
+      pending.push_back(m);
+      if (off + m->nnz > capacity)
+        fail(SPGEMM_INVALID_ARGUMENT, "spgemm_multiply_into: C has more than the " + std::to_string(capacity) +
+                                          " entries the output buffers hold");
+      if (off != 0 && m->rows + 1 > 0) {
+        const int grid = static_cast<int>(std::min<int64_t>(ctx->num_sms * 4, ceil_div(m->rows + 1, 256)));
+        k_add_offset<<<std::max(grid, 1), 256, 0, ctx->main_s>>>(m->rpt, m->rpt, m->rows + 1, off);
+        ck(cudaGetLastError(), "k_add_offset");
+        ctx->launches.fetch_add(1);
+      }
+      const spgemm_status s3 =
+          spgemm_matrix_download_async(ctx, m, rpt + r0, col ? col + off : nullptr, val ? val + off : nullptr, 1);
+      if (s3 != SPGEMM_OK) fail(s3, g_err);
+      off += m->nnz;
+      if (dbg) std::fprintf(stderr, "into: block %d rows [%lld,%lld) nnz %lld issued at %.2f ms\n", i,
+                            static_cast<long long>(r0), static_cast<long long>(r1), static_cast<long long>(m->nnz),
+                            ms_since());
+      if (first) {
+        combined = rep;
+        first = false;
+      } else {
+        combined.total_nprod += rep.total_nprod;
+        combined.spilled_rows += rep.spilled_rows;
+        combined.max_nnz_per_row = std::max(combined.max_nnz_per_row, rep.max_nnz_per_row);
+        combined.timings.total += rep.timings.total;
+        combined.metadata_calls += rep.metadata_calls;
+        combined.metadata_bytes += rep.metadata_bytes;
+        combined.output_calls += rep.output_calls;
+        combined.output_bytes += rep.output_bytes;
+      }
+    }
+    ck(cudaStreamSynchronize(ctx->side_s), "cudaStreamSynchronize(copy lane)");
+    if (dbg) std::fprintf(stderr, "into: downloads done at %.2f ms\n", ms_since());
+    if (M == 0) rpt[0] = 0;
+    for (spgemm_matrix* m : pending) spgemm_matrix_free(m);
+    pending.clear();
+    combined.rows = M;
+    combined.nnz = a_nnz;
+    combined.nnz_per_row_mean = M > 0 ? static_cast<double>(a_nnz) / static_cast<double>(M) : 0.0;
+    combined.nnz_of_product = off;
+    combined.cr = off > 0 ? static_cast<double>(combined.total_nprod) / static_cast<double>(off) : 0.0;
+    if (nnz_out) *nnz_out = off;
+    if (report) *report = combined;
+  });
+  cleanup();
   return st;
 }
 

@@ -606,6 +606,30 @@ __global__ void __launch_bounds__(kBinThreads)
   }
 }
 
+// Phase scalars to pinned, mapped host memory: written by the SMs rather than
+// by a copy engine, so the read-back never queues behind a large device->host
+// transfer on the copy lane (multiply_into's downloads).
+static_assert(sizeof(DevInfo) % 8 == 0, "DevInfo moves as 8-byte words");
+__global__ void k_info_to_host(const DevInfo* __restrict__ src, DevInfo* dst, int count) {
+  const int words = count * static_cast<int>(sizeof(DevInfo) / 8);
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+  volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(dst);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
+  __threadfence_system();
+}
+
+__global__ void k_read_i64(const int64_t* __restrict__ src, volatile int64_t* dst) {
+  *dst = *src;
+  __threadfence_system();
+}
+
+// dst[i] = src[i] + delta (row-pointer rebasing of row blocks; dst may be src)
+__global__ void k_add_offset(int64_t* dst, const int64_t* src, int64_t n, int64_t delta) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i] + delta;
+}
+
 __global__ void k_iota(int64_t* out, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
