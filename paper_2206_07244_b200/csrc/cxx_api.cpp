@@ -545,4 +545,14 @@ NnzForecast forecast_nnz(const CsrMatrix& a, const CsrMatrix& b, const SpgemmOpt
   return f;
 }
 
+std::int64_t multiply_into(const CsrMatrix& a, const CsrMatrix& b, offset_t* rpt, index_t* col, double* val,
+                           std::int64_t capacity, const SpgemmOptions& options, int parts) {
+  spgemm_ctx* ctx = ctx_for(0);
+  const spgemm_options o = to_c_options(options);
+  const spgemm_csr_view va = view(a), vb = view(b);
+  std::int64_t nnz = 0;
+  ok(spgemm_multiply_into(ctx, &va, &vb, &o, parts, rpt, capacity, col, val, &nnz, nullptr));
+  return nnz;
+}
+
 }  // namespace spgemm
