@@ -183,8 +183,6 @@ struct spgemm_ctx {
   cudaEvent_t ev_join[kNumBins] = {};
   DevInfo* h_info = nullptr;      // pinned and mapped, two slots
   DevInfo* h_info_dev = nullptr;  // h_info's device address (written by k_info_to_host)
-  int64_t* h_scalar = nullptr;    // pinned and mapped scalar (k_read_i64)
-  int64_t* h_scalar_dev = nullptr;
   std::atomic<int64_t> launches{0};
   std::mutex attr_mu;
   std::unordered_set<const void*> attr_done;
@@ -373,6 +371,15 @@ struct spgemm_pipeline {
   uint32_t scale = 107;
   double avg_b_len = 0;
   bool idx32 = true;
+  int64_t b_rows = 0;
+  // operand sizes: known at creation for host operands, from K1 for device ones
+  void set_sizes() {
+    // 32-bit B/A offsets in the group and heap kernels when every offset fits;
+    // SPGEMM_FORCE_IDX64=1 takes the 64-bit kernels regardless (test coverage of
+    // the path inputs above 2^31 nonzeros take)
+    idx32 = a_nnz < (int64_t(1) << 31) && b_nnz < (int64_t(1) << 31) && std::getenv("SPGEMM_FORCE_IDX64") == nullptr;
+    avg_b_len = b_rows > 0 ? static_cast<double>(b_nnz) / static_cast<double>(b_rows) : 0;
+  }
   bool sym_bins_on_device = false;
 
   int64_t* d_rpt = nullptr;
@@ -458,12 +465,9 @@ void stage_input(spgemm_ctx* ctx, const spgemm_csr_view* v, DevCsr* d, void** ow
       ck(cudaStreamWaitEvent(ctx->main_s, e, 0), "main waits for default stream");
       ctx->ev_pool.push_back(e);
     }
-    // nnz = rpt[rows], read by an SM into mapped host memory (a copy-engine
-    // read-back would queue behind downloads in flight on the copy lane)
-    SPG_LAUNCH(ctx, "k_read_i64", ctx->main_s,
-               k_read_i64<<<1, 1, 0, ctx->main_s>>>(v->rpt + v->rows, ctx->h_scalar_dev));
-    ck(cudaStreamSynchronize(ctx->main_s), "cudaStreamSynchronize");
-    *nnz = *const_cast<volatile int64_t*>(ctx->h_scalar);
+    // nnz = rpt[rows] stays on the device: K1 reports it with its phase
+    // scalars (no extra host round trip per operand)
+    *nnz = -1;
     d->rpt = v->rpt;
     d->col = v->col;
     d->val = v->val;
@@ -507,12 +511,15 @@ void spgemm_pipeline::setup() {
   ck(cudaMemsetAsync(d_info_sym, 0, 2 * sizeof(DevInfo), s), "memset info");
   if (M > 0) {
     SPG_LAUNCH(ctx, "k_setup_nprod", s,
-               k_setup_nprod<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(A, B.rpt, d_rpt, M, sym_up,
+               k_setup_nprod<<<static_cast<unsigned>(nrb), kBinThreads, 0, s>>>(A, B.rpt, b_rows, d_rpt, M, sym_up,
                                                                       d_blk, d_info_sym));
   } else {
     ck(cudaMemsetAsync(d_rpt, 0, 8, s), "memset rpt");
   }
   fetch_info(d_info_sym, &h_sym);
+  if (a_nnz < 0) a_nnz = M > 0 ? h_sym.a_nnz : 0;
+  if (b_nnz < 0) b_nnz = M > 0 ? h_sym.b_nnz : 0;
+  set_sizes();
   if (h_sym.total > static_cast<unsigned long long>(std::numeric_limits<int64_t>::max()))
     fail(SPGEMM_OVERFLOW, "spgemm: intermediate-product count overflowed 64 bits");
   total_nprod = static_cast<int64_t>(h_sym.total);
@@ -995,9 +1002,6 @@ spgemm_status spgemm_ctx_create(int32_t device, spgemm_ctx** out) {
       ck(cudaHostAlloc(&c->h_info, 2 * sizeof(DevInfo), cudaHostAllocMapped | cudaHostAllocPortable),
          "cudaHostAlloc");
       ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_info_dev), c->h_info, 0), "cudaHostGetDevicePointer");
-      ck(cudaHostAlloc(&c->h_scalar, 64, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
-      ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_scalar_dev), c->h_scalar, 0),
-         "cudaHostGetDevicePointer");
       // Keep freed blocks in the stream-ordered pool: repeated multiplies
       // reuse HBM without returning it to the driver.
       cudaMemPool_t pool;
@@ -1039,7 +1043,6 @@ void spgemm_ctx_destroy(spgemm_ctx* c) {
   for (auto& e : c->ev_pool) cudaEventDestroy(e);
   for (auto& b : c->scratch) cudaFree(b.p);
   if (c->h_info) cudaFreeHost(c->h_info);
-  if (c->h_scalar) cudaFreeHost(c->h_scalar);
   if (prev >= 0) cudaSetDevice(prev);
   delete c;
 }
@@ -1153,12 +1156,7 @@ spgemm_status spgemm_pipeline_create(spgemm_ctx* ctx, const spgemm_csr_view* a,
         stage_input(ctx, b, &p->B, p->owned + 3, &p->b_nnz);
       }
       p->M = a->rows;
-      // 32-bit B/A offsets in the group and heap kernels when every offset fits;
-      // SPGEMM_FORCE_IDX64=1 takes the 64-bit kernels regardless (test coverage of
-      // the path inputs above 2^31 nonzeros take)
-      p->idx32 = p->a_nnz < (int64_t(1) << 31) && p->b_nnz < (int64_t(1) << 31) &&
-                 std::getenv("SPGEMM_FORCE_IDX64") == nullptr;
-      p->avg_b_len = b->rows > 0 ? static_cast<double>(p->b_nnz) / static_cast<double>(b->rows) : 0;
+      p->b_rows = b->rows;
       for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     } catch (...) {
       spgemm_pipeline_destroy(p);

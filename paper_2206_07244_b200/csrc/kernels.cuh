@@ -61,6 +61,7 @@ struct DevInfo {
   unsigned long long spill_count;
   long long scan_total;
   long long a_max_row;           // max nnz per A row (input_stats)
+  long long a_nnz, b_nnz;        // A.rpt[M], B.rpt[B.rows] (device operands: read by K1)
   int tile_counter;
   int pad_;
 };
@@ -371,11 +372,15 @@ __device__ __forceinline__ void pass1_finish(int* s_hist, long long mx, unsigned
 // Rows are read coalesced (thread per row); rows longer than 32 entries are
 // summed cooperatively by their warp so power-law rows do not serialise.
 __global__ void __launch_bounds__(kBinThreads)
-    k_setup_nprod(DevCsr A, const int64_t* __restrict__ brpt, int64_t* __restrict__ rpt,
+    k_setup_nprod(DevCsr A, const int64_t* __restrict__ brpt, int64_t b_rows, int64_t* __restrict__ rpt,
                   int64_t M, BinUpper up, int32_t* __restrict__ blk_counts, DevInfo* info) {
   __shared__ int s_hist[kNumBins];
   __shared__ long long s_red[16];
   if (threadIdx.x < kNumBins) s_hist[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // operand sizes, so the host never reads them separately
+    info->a_nnz = A.rpt[M];
+    info->b_nnz = brpt[b_rows];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
@@ -615,11 +620,6 @@ __global__ void k_info_to_host(const DevInfo* __restrict__ src, DevInfo* dst, in
   const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
   volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(dst);
   for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
-  __threadfence_system();
-}
-
-__global__ void k_read_i64(const int64_t* __restrict__ src, volatile int64_t* dst) {
-  *dst = *src;
   __threadfence_system();
 }
 
