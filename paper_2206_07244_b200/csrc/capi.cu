@@ -167,6 +167,10 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 #endif
 // 8-lane groups when B's rows average at most this many entries (else 32)
 constexpr double kG8MaxBLen = SPGEMM_G8_MAX;
+#ifndef SPGEMM_THREAD_SLOTS
+#define SPGEMM_THREAD_SLOTS 24
+#endif
+constexpr int kThreadNumSlots = SPGEMM_THREAD_SLOTS;  // k_num_thread's per-row table (>= 1.5 x 16)
 constexpr int64_t kSpecBudget = int64_t(4) << 30;      // scratch bytes the arena may spend on it
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -814,12 +818,13 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     SPG_LAUNCH(ctx, "k_num_global", s,
                k_num_global<<<gblocks, kGlobalThreads, 0, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, gkeys,
                                                     gvals, gbits, gslots, gwords, d_info_num));
-  } else if (u <= 16) {  // thread per row: 32-slot private table, 16-key register sort
-    const size_t smem = 128 * 32 * 12;
-    auto kern = &k_num_thread<32, 16>;
+  } else if (u <= 16) {  // thread per row: 24-slot private table, 16-key register sort
+    constexpr int TS = kThreadNumSlots;
+    const size_t smem = 128 * TS * 12;
+    auto kern = &k_num_thread<TS, 16>;
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, 128, smem, ceil_div(rl.count, 128));
-    SPG_LAUNCH(ctx, "k_num_thread<32,16>", s,
+    SPG_LAUNCH(ctx, "k_num_thread<" + std::to_string(TS) + ",16>", s,
                kern<<<grid, 128, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec));
   } else if (u <= 32) {
     if (g8) group(NUMG(8, 64, 4, 32), 8, 64, 4, 32);

@@ -1176,7 +1176,9 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Thread-per-row numeric kernel for rows with nnz <= NMAX (TS = 2*NMAX slots):
+// Thread-per-row numeric kernel for rows with nnz <= NMAX (TS >= 1.5*NMAX slots,
+// any TS: the home slot is the high product of the Fibonacci hash and TS, so a
+// 24-slot table (288 B/thread instead of 384) fits 6 blocks per SM instead of 4):
 // the thread walks its row in the reference's order (so the fold is trivially
 // the reference's), compacts its private table in place, sorts the NMAX packed
 // (col, slot) keys with a register bitonic network, and writes C(i,:).
@@ -1191,7 +1193,8 @@ __global__ void __launch_bounds__(128)
   double* vals = reinterpret_cast<double*>(smem_raw) + warp * TS * 32 + lane;
   int32_t* keys = reinterpret_cast<int32_t*>(smem_raw + static_cast<size_t>(blockDim.x) * TS * 8) +
                   warp * TS * 32 + lane;
-  const Hash hs = make_hash(scale, log2_const<TS>());
+  const Hash hs = make_hash(scale, 5);  // its multiplier; the slot range is TS
+  auto home = [&](int32_t key) { return __umulhi(static_cast<uint32_t>(key) * hs.mult, static_cast<uint32_t>(TS)); };
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rl.count; idx += stride) {
     const int64_t row = rl.row(idx);
@@ -1218,7 +1221,7 @@ __global__ void __launch_bounds__(128)
       const int64_t q0 = B.rpt[k0], e0 = B.rpt[k0 + 1];
       const int64_t q1 = B.rpt[k1], e1 = two ? B.rpt[k1 + 1] : q1;
       auto insert = [&](int32_t key, double x) {
-        uint32_t h = hs.home(key);
+        uint32_t h = home(key);
         while (true) {
           const int32_t c = keys[h * 32];
           if (c == key) break;
@@ -1226,7 +1229,7 @@ __global__ void __launch_bounds__(128)
             keys[h * 32] = key;
             break;
           }
-          h = (h + 1) & (TS - 1);
+          h = h + 1 == TS ? 0u : h + 1;
         }
         vals[h * 32] = __dadd_rn(vals[h * 32], x);
       };
