@@ -171,6 +171,10 @@ constexpr double kG8MaxBLen = SPGEMM_G8_MAX;
 #define SPGEMM_THREAD_SLOTS 24
 #endif
 constexpr int kThreadNumSlots = SPGEMM_THREAD_SLOTS;  // k_num_thread's per-row table (>= 1.5 x 16)
+#ifndef SPGEMM_THREAD_SYM_SLOTS
+#define SPGEMM_THREAD_SYM_SLOTS 48
+#endif
+constexpr int kThreadSymSlots = SPGEMM_THREAD_SYM_SLOTS;  // k_sym_thread's per-row table (>= 1.5 x 32)
 constexpr int64_t kSpecBudget = int64_t(4) << 30;      // scratch bytes the arena may spend on it
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -662,12 +666,14 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     dev_free(pool, s);
     return;
   }
-  if (u <= 32) {  // thread per row, private 64-slot table (load <= 1/2)
-    const size_t smem = 256 * 64 * 4;
-    auto kern = &k_sym_thread<64>;
+  if (u <= 32) {  // thread per row, private table of 1.5 x 32 slots (load <= 2/3)
+    constexpr int TS = kThreadSymSlots;
+    const size_t smem = 256 * TS * 4;
+    auto kern = &k_sym_thread<TS>;
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, 256, smem, ceil_div(rl.count, 256));
-    SPG_LAUNCH(ctx, "k_sym_thread<64>", s, kern<<<grid, 256, smem, s>>>(rl, A, B, d_rpt, scale));
+    SPG_LAUNCH(ctx, "k_sym_thread<" + std::to_string(TS) + ">", s,
+               kern<<<grid, 256, smem, s>>>(rl, A, B, d_rpt, scale));
     return;
   }
   // group kernels: (G, T, groups per block, bitmap words per group)

@@ -1134,7 +1134,8 @@ __global__ void __launch_bounds__(G* NGRP)
   }
 }
 
-// Thread-per-row symbolic kernel for the smallest bin (nprod <= TS/2): each
+// Thread-per-row symbolic kernel for the smallest bin (nprod <= 2*TS/3; any TS,
+// home slot = high product of the Fibonacci hash and TS): each
 // thread owns one row and a private TS-slot table in shared memory laid out
 // interleaved (slot s of lane l at [s*32 + l]: every lane always hits its own
 // bank, whatever slot it probes). No atomics, barriers or shuffles.
@@ -1145,7 +1146,8 @@ __global__ void __launch_bounds__(256)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t* tab = reinterpret_cast<int32_t*>(smem_raw) + warp * TS * 32 + lane;
-  const Hash hs = make_hash(scale, log2_const<TS>());
+  const Hash hs = make_hash(scale, 5);  // its multiplier; the slot range is TS
+  auto home = [&](int32_t key) { return __umulhi(static_cast<uint32_t>(key) * hs.mult, static_cast<uint32_t>(TS)); };
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rl.count; idx += stride) {
     const int64_t row = rl.row(idx);
@@ -1159,7 +1161,7 @@ __global__ void __launch_bounds__(256)
       const int64_t b1 = B.rpt[k + 1];
       for (int64_t q = B.rpt[k]; q < b1; ++q) {
         const int32_t key = B.col[q];
-        uint32_t h = hs.home(key);
+        uint32_t h = home(key);
         while (true) {
           const int32_t c = tab[h * 32];
           if (c == key) break;
@@ -1168,7 +1170,7 @@ __global__ void __launch_bounds__(256)
             ++cnt;
             break;
           }
-          h = (h + 1) & (TS - 1);
+          h = h + 1 == TS ? 0u : h + 1;
         }
       }
     }
