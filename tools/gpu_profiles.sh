@@ -12,6 +12,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/${R}_launches_config2.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_num_group|k_sym_group" -c 3 -f \
   -o gpurun_out/${R}_full_config2 python tools/prof_run.py 2 1 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_num_thread|k_sym_thread" -c 2 -f \
+  -o gpurun_out/${R}_full_config1 python tools/prof_run.py 1 1 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_num_group|k_num_thread" -c 4 -f \
+  -o gpurun_out/${R}_full_config4 python tools/prof_run.py 4 1 > /dev/null 2>&1
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_big_sym" -c 1 -f \
   -o gpurun_out/${R}_full_config3_sym python tools/prof_run.py 3 1 > /dev/null 2>&1
 timeout 1800 ncu --set full --import-source on --clock-control none -k regex:"k_big_num" -c 1 -f \
