@@ -92,6 +92,28 @@ def test_no_gpu_fails_loudly_here(sg):
         sg.multiply(a, a)
 
 
+def test_new_entry_points_fail_loudly_without_gpu(sg):
+    """forecast_nnz / multiply_into validate their arguments on the host and then refuse
+    to run without an sm_100 device (no CPU fallback)."""
+    from conftest import HAS_GPU
+    if HAS_GPU:
+        pytest.skip("GPU present")
+    import numpy as np
+    a = sg.CsrMatrix(2, 2, [0, 1, 2], [0, 1], [1.0, 1.0])
+    b = sg.CsrMatrix(3, 2, [0, 1, 2, 2], [0, 1], [1.0, 1.0])
+    with pytest.raises(sg.InvalidArgument):
+        sg.forecast_nnz(a, b)  # a.cols != b.rows
+    rpt, col, val = np.zeros(3, np.int64), np.zeros(4, np.int32), np.zeros(4)
+    with pytest.raises(sg.InvalidArgument):
+        sg.multiply_into(a, a, rpt.astype(np.int32), col, val)  # wrong rpt dtype
+    with pytest.raises(sg.InvalidArgument):
+        sg.multiply_into(a, a, np.zeros(2, np.int64), col, val)  # rpt too short
+    with pytest.raises(sg.NoDevice):
+        sg.multiply_into(a, a, rpt, col, val)
+    with pytest.raises(sg.NoDevice):
+        sg.forecast_nnz(a, a)
+
+
 def test_validate_csr_reports_violations(sg):  # test_csr.cpp validation messages
     good = sg.CsrMatrix(2, 3, [0, 2, 3], [0, 2, 1], [1.0, 2.0, 3.0])
     assert sg.validate_csr(good).ok()
