@@ -619,8 +619,8 @@ __global__ void k_info_to_host(const DevInfo* __restrict__ src, DevInfo* dst, in
   const int words = count * static_cast<int>(sizeof(DevInfo) / 8);
   const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
   volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(dst);
+  // kernel completion + the host's stream synchronisation make the writes visible
   for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
-  __threadfence_system();
 }
 
 // dst[i] = src[i] + delta (row-pointer rebasing of row blocks; dst may be src)
