@@ -445,7 +445,8 @@ def main():
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": kernel_bytes, "avg_launch_ms": avg_s * 1e3,
-                "share_of_step": ms_total / t_prof_ms, "profiled_pass_ms_per_step": t_prof_ms / args.steps}
+                "share_of_step": ms_total / t_prof_ms, "profiled_pass_ms_per_step": t_prof_ms / args.steps,
+                "profiled_pass": "second timed pass with per-launch events; bins serialised on one stream so each launch is timed alone"}
         step_roof = {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,
                      "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
 

@@ -138,8 +138,10 @@ spgemm_status spgemm_ctx_synchronize(spgemm_ctx* ctx);
 void* spgemm_ctx_stream(spgemm_ctx* ctx);
 
 /* Per-kernel device time: when profiling is on, every launch is bracketed by
- * CUDA events on the stream it is launched on. The summary (aggregated by
- * kernel name, then cleared) synchronises the device. */
+ * CUDA events on the stream it is launched on, and the per-bin kernels run in
+ * order on the context's main stream (not concurrently) so each launch is timed
+ * alone. The summary (aggregated by kernel name, then cleared) synchronises the
+ * device. */
 typedef struct spgemm_kernel_time {
   char name[48];
   int64_t launches;

@@ -308,6 +308,11 @@ struct LaunchScope {
     ls_.done();                                  \
   } while (0)
 
+// Bins run concurrently on their own streams; with per-launch profiling on they
+// run in order on the main stream, so each launch's events time that kernel alone
+// (concurrent bins would fold their co-resident neighbours into its duration).
+cudaStream_t bin_stream(spgemm_ctx* ctx, int bin) { return ctx->prof ? ctx->main_s : ctx->bin_s[bin]; }
+
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
@@ -708,7 +713,7 @@ void spgemm_pipeline::run_symbolic() {
   for (int r = 0; r < kNumBins; ++r) {
     const int bin = sym_plan.launch_order[r];
     if (sym_bins_on_device ? bin > top : bin_info.bin_size[bin] == 0) continue;
-    cudaStream_t s = ctx->bin_s[bin];
+    cudaStream_t s = bin_stream(ctx, bin);
     ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
     // device-resolved row list: `count` only sizes the persistent grid
     RowList rl = sym_bins_on_device
@@ -884,7 +889,7 @@ void spgemm_pipeline::run_numeric() {
   for (int r = 0; r < kNumBins; ++r) {
     const int bin = num_plan.launch_order[r];
     if (bin_info.bin_size[bin] == 0) continue;
-    cudaStream_t s = ctx->bin_s[bin];
+    cudaStream_t s = bin_stream(ctx, bin);
     ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
     RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path, nullptr, bin};
     launch_num_bin(bin, rl, s, gkeys, gvals, gbits, gslots, gwords, gblocks);
