@@ -59,16 +59,18 @@ typedef struct spgemm_options {
   char num_preset[16];     /* "num_1x" | "num_1.5x" | "num_2x" | "num_3x"  */
   int32_t workers;         /* CPU pool size in the reference; reported only */
   int32_t overlap;         /* stream-ordered C allocation overlap on/off    */
-  int32_t deterministic;   /* stable (1) or unordered (0) bin scatter       */
+  int32_t deterministic;   /* 1: C bitwise reproducible and equal to the
+                              reference's summation order on every row
+                              (SPEC.md:394); 0: heap-tier rows (bin 7) may
+                              accumulate with fp64 atomics (within 1e-12)     */
   int64_t chunk_rows;      /* CPU task granularity in the reference; unused */
   int64_t hash_scale;      /* HashParams::hash_scale, positive odd          */
   int32_t has_sym_launch_order;
   int32_t sym_launch_order[SPGEMM_NUM_BINS];
   int32_t has_num_launch_order;
   int32_t num_launch_order[SPGEMM_NUM_BINS];
-  int32_t ordered_heap;    /* B200 extension: 1 = heap-tier rows (numeric bin 7)
-                              fold in the reference's order (bitwise, slower);
-                              0 = bitmap rank + fp64 atomics (within 1e-12)   */
+  int32_t ordered_heap;    /* B200 extension: 1 = heap-tier rows fold in the
+                              reference's order even when deterministic = 0  */
 } spgemm_options;
 
 /* StepTimings (pipeline.hpp:93-102), seconds, measured with CUDA events. */

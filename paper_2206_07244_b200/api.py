@@ -462,8 +462,10 @@ class SpgemmOptions:
     alloc_stats: Optional[AllocStats] = None
     sym_launch_order: Optional[Sequence[int]] = None
     num_launch_order: Optional[Sequence[int]] = None
-    # B200 extension: fold heap-tier rows (numeric bin 7) in the reference's
-    # order -- bitwise equal, slower; default: bitmap rank + fp64 atomics (1e-12)
+    # deterministic=True (default): every row, heap tier included, folds in the
+    # reference's order (bitwise); deterministic=False lets heap-tier rows
+    # accumulate with fp64 atomics (1e-12). B200 extension: ordered_heap forces
+    # the ordered heap tier even with deterministic=False.
     ordered_heap: bool = False
 
     def _c(self) -> _c.Options:

@@ -453,9 +453,14 @@ struct spgemm_pipeline {
   void launch_num_bin(int bin, const RowList& rl, cudaStream_t s, int32_t* gkeys, double* gvals,
                       uint32_t* gbits, int64_t gslots, int64_t gwords, int gblocks);
   void release(bool keep_result);
-  // heap-tier numeric: bitmap + rank with fp64 atomics (default), or the
-  // ordered per-A-entry kernel (options.ordered_heap: bitwise summation order)
-  bool heap_bitmap() const { return idx32 && !opts.ordered_heap; }
+  // heap-tier numeric: the ordered kernel whenever the reference's determinism
+  // contract applies (options.deterministic, the default: C bitwise the
+  // reference's) or options.ordered_heap forces it; bitmap rank +
+  // fp64 atomics (within 1e-12, run-to-run bits may differ) only for
+  // deterministic=false
+  bool heap_ordered() const { return opts.ordered_heap || opts.deterministic; }
+  bool heap_bitmap() const { return idx32; }  // bitmap kernels (ordered or atomic); else k_num_global
+  int32_t* d_poff = nullptr;                   // ordered bitmap tier: B's column-panel offsets
 };
 
 namespace {
@@ -820,7 +825,13 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     SPG_LAUNCH(ctx, "k_num_block<" + std::to_string(T) + ">", s,
                kern<<<grid, threads, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
   };
-  if ((bin == kNumBins - 1 || u > 4096) && heap_bitmap()) {
+  if ((bin == kNumBins - 1 || u > 4096) && heap_bitmap() && heap_ordered()) {
+    prepare_kernel(ctx, k_big_num_ord, kBigNumSmem);
+    const int grid = persistent_grid(ctx, k_big_num_ord, kBigThreads, kBigNumSmem, rl.count);
+    SPG_LAUNCH(ctx, "k_big_num_ord", s,
+               k_big_num_ord<<<grid, kBigThreads, kBigNumSmem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, d_poff,
+                                                                    d_info_num));
+  } else if ((bin == kNumBins - 1 || u > 4096) && heap_bitmap()) {
     prepare_kernel(ctx, k_big_num, kBigNumSmem);
     const int grid = persistent_grid(ctx, k_big_num, kBigThreads, kBigNumSmem, rl.count);
     SPG_LAUNCH(ctx, "k_big_num", s,
@@ -880,6 +891,32 @@ void spgemm_pipeline::run_numeric() {
     gvals = static_cast<double*>(dev_alloc(static_cast<size_t>(gslots) * 8 * gblocks, ctx->main_s));
     gbits = static_cast<uint32_t*>(dev_alloc(static_cast<size_t>(gwords) * 8 * gblocks, ctx->main_s));
   }
+  // Ordered bitmap tier: B's column panels (one per warp of the row's block),
+  // balanced by B's column counts, and every B row's panel boundaries.
+  unsigned char* panel_buf = nullptr;
+  if (grows > 0 && heap_bitmap() && heap_ordered()) {
+    const size_t o_colb = align_up(static_cast<size_t>(kHistBuckets) * 8, 256);
+    const size_t o_poff = align_up(o_colb + (kPanels + 1) * 4, 256);
+    const size_t bytes = o_poff + static_cast<size_t>(B.rows) * (kPanels + 1) * 4;
+    panel_buf = static_cast<unsigned char*>(dev_alloc(bytes, ctx->main_s));
+    auto* hist = reinterpret_cast<unsigned long long*>(panel_buf);
+    auto* colb = reinterpret_cast<int32_t*>(panel_buf + o_colb);
+    d_poff = reinterpret_cast<int32_t*>(panel_buf + o_poff);
+    const int64_t bw = std::max<int64_t>(1, ceil_div(B.cols, kHistBuckets));
+    ck(cudaMemsetAsync(hist, 0, static_cast<size_t>(kHistBuckets) * 8, ctx->main_s), "memset hist");
+    if (b_nnz > 0) {
+      const int hg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 4, ceil_div(b_nnz, 256)));
+      SPG_LAUNCH(ctx, "k_col_hist", ctx->main_s,
+                 k_col_hist<<<std::max(hg, 1), 256, 0, ctx->main_s>>>(B.col, b_nnz, bw, hist));
+    }
+    SPG_LAUNCH(ctx, "k_panel_bounds", ctx->main_s,
+               k_panel_bounds<<<1, 1024, 0, ctx->main_s>>>(hist, bw, B.cols, colb));
+    if (B.rows > 0) {
+      const int sg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 16, ceil_div(B.rows, 8)));
+      SPG_LAUNCH(ctx, "k_panel_split", ctx->main_s,
+                 k_panel_split<<<std::max(sg, 1), 256, 0, ctx->main_s>>>(B, colb, d_poff));
+    }
+  }
   if (spec.flag != nullptr && M > 0) {
     const int grid = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(M, 256)));
     SPG_LAUNCH(ctx, "k_spec_copy", ctx->main_s,
@@ -889,7 +926,9 @@ void spgemm_pipeline::run_numeric() {
   for (int r = 0; r < kNumBins; ++r) {
     const int bin = num_plan.launch_order[r];
     if (bin_info.bin_size[bin] == 0) continue;
-    cudaStream_t s = bin_stream(ctx, bin);
+    // the heap-tier bins share the k_num_global pool: one stream for them
+    const bool heap_bin = bin == kNumBins - 1 || num_plan.config.upper[bin] > 4096;
+    cudaStream_t s = heap_bin && !heap_bitmap() ? ctx->main_s : bin_stream(ctx, bin);
     ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
     RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path, nullptr, bin};
     launch_num_bin(bin, rl, s, gkeys, gvals, gbits, gslots, gwords, gblocks);
@@ -899,6 +938,8 @@ void spgemm_pipeline::run_numeric() {
   dev_free(gkeys, ctx->main_s);
   dev_free(gvals, ctx->main_s);
   dev_free(gbits, ctx->main_s);
+  dev_free(panel_buf, ctx->main_s);
+  d_poff = nullptr;
   mark(11);
   stage = kNumeric;
 }

@@ -325,4 +325,233 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ordered heap tier (deterministic=true, the default): the same bitmap + rank
+// directory as k_big_num, but pass B keeps the reference's per-column
+// summation order, ((0 + a[i,k0]*b[k0,c]) + a[i,k1]*b[k1,c]) + ... in A-row
+// order (hash_tables.cpp:182-193), so C is bitwise the reference's.
+//
+// Order needs one owner per output column. B's columns are split once per
+// product into kPanels column panels balanced by B's column counts
+// (k_col_hist + k_panel_bounds), and every B row's panel boundaries are stored
+// (k_panel_split: poff[k*(kPanels+1) + p] = first entry of row k in panel p).
+// Warp w of the row's block owns panel w: it walks the whole A row in order,
+// 32 entries at a time, takes only its panel's slice of each B row (two loads
+// per entry, no search), flattens the slices into rounds of 32 consecutive
+// products (A order, then B order) and adds each product into C.val at its
+// rank with a plain read-modify-write. Within a round, products of one entry
+// have distinct columns; when a round spans several entries, lanes holding the
+// same column (__match_any_sync) fold in lane order -- which is A order -- the
+// group's first lane starting from C.val and each next lane adding to its
+// predecessor's sum. Rounds are separated by __syncwarp, and no other warp
+// ever touches the panel's columns, so every column is folded sequentially in
+// A order. No atomics, no zeroing race: pass A zeroes C.val before the block
+// barrier that precedes pass B.
+constexpr int kPanels = kBigWarps;  // one column panel per warp
+constexpr int kHistBuckets = 4096;
+
+// Histogram of B's columns over kHistBuckets equal-width buckets.
+__global__ void __launch_bounds__(256)
+    k_col_hist(const int32_t* __restrict__ col, int64_t nnz, int64_t bucket_w,
+               unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[kHistBuckets];
+  for (int i = threadIdx.x; i < kHistBuckets; i += blockDim.x) h[i] = 0u;
+  __syncthreads();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride)
+    atomicAdd(&h[min(static_cast<int64_t>(kHistBuckets - 1), col[e] / bucket_w)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBuckets; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(h[i]));
+}
+
+// Panel p starts at the first bucket boundary where the cumulative count
+// reaches p/kPanels of B's nonzeros (one block).
+__global__ void __launch_bounds__(1024)
+    k_panel_bounds(const unsigned long long* __restrict__ hist, int64_t bucket_w, int64_t ncols,
+                   int32_t* __restrict__ colb) {
+  __shared__ long long red[32];
+  constexpr int PER = kHistBuckets / 1024;
+  long long mine = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) mine += static_cast<long long>(hist[threadIdx.x * PER + i]);
+  long long total;
+  long long run = block_exclusive_scan<1024>(mine, red, &total);
+  if (threadIdx.x == 0) {
+    colb[0] = 0;
+    colb[kPanels] = static_cast<int32_t>(min(ncols, static_cast<int64_t>(0x7fffffff)));
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int b = threadIdx.x * PER + i;
+    const long long before = run;
+    run += static_cast<long long>(hist[b]);
+    // panel p (1..P-1) begins at bucket b when the cumulative count crosses p*total/P within it
+    for (int p = 1; p < kPanels; ++p) {
+      const long long target = total * p / kPanels;
+      if (before < target && run >= target) colb[p] = static_cast<int32_t>(min(ncols, (b + 1) * bucket_w));
+      if (total == 0 && b == 0) colb[p] = static_cast<int32_t>(min(ncols, p * (ncols / kPanels)));
+    }
+  }
+}
+
+// poff[k*(kPanels+1) + p] = first entry of B row k with column >= colb[p]
+// (warp per row, lane p binary-searches boundary p; lane 0 = row start).
+__global__ void __launch_bounds__(256)
+    k_panel_split(DevCsr B, const int32_t* __restrict__ colb, int32_t* __restrict__ poff) {
+  const int lane = threadIdx.x & 31;
+  const int32_t bound = colb[lane];
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < B.rows; k += warps) {
+    const int64_t r0 = B.rpt[k], r1 = B.rpt[k + 1];
+    int64_t lo = r0, hi = r1;  // first index with col >= bound
+    if (lane == 0) hi = r0;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (B.col[mid] < bound) lo = mid + 1;
+      else hi = mid;
+    }
+    int32_t* out = poff + k * (kPanels + 1);
+    out[lane] = static_cast<int32_t>(lo);
+    if (lane == 0) out[kPanels] = static_cast<int32_t>(r1);
+  }
+}
+
+__global__ void __launch_bounds__(kBigThreads, 1)
+    k_big_num_ord(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
+                  double* __restrict__ cval, const int32_t* __restrict__ poff, DevInfo* info) {
+  const RowList rl = rl_in.resolved();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
+  uint16_t* pre = reinterpret_cast<uint16_t*>(smem_raw + sizeof(uint32_t) * kBigWordsPad);
+  uint32_t* sup =
+      reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint32_t) * kBigWordsPad + sizeof(uint16_t) * kBigPrePad);
+  BigTile& t = *reinterpret_cast<BigTile*>(smem_raw + sizeof(uint32_t) * kBigWordsPad +
+                                           sizeof(uint16_t) * kBigPrePad + sizeof(uint32_t) * (kBigWords / kBigSuper));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
+    const int64_t row = rl.row(idx);
+    const int64_t base = rpt[row];
+    const int64_t n = rpt[row + 1] - base;
+    if (n == 0) continue;
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    int64_t woff = 0;
+    for (int64_t wc0 = 0; wc0 < B.cols; wc0 += kBigWindow) {
+      uint4* b4 = reinterpret_cast<uint4*>(bm);
+      for (int s = tid; s < kBigWordsPad / 4; s += kBigThreads) b4[s] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+      const int32_t c0 = static_cast<int32_t>(wc0);
+      // ---- pass A: the window's column set (as k_big_num)
+      big_walk<false>(A, B, a0, a1, t, [&](int32_t col, double, bool valid) {
+        const uint32_t off = static_cast<uint32_t>(col - c0);
+        if (valid && off < static_cast<uint32_t>(kBigWindow)) atomicOr(bm + bm_idx(off >> 5), 1u << (off & 31u));
+      });
+      // ---- rank directory; C.col from the bitmap; C.val zeroed
+      const int w0 = tid * kBigWordsPerThread;
+      int mine = 0;
+#pragma unroll 8
+      for (int i = 0; i < kBigWordsPerThread; ++i) mine += __popc(bm[bm_idx(w0 + i)]);
+      long long wtot;
+      const long long g = block_exclusive_scan<kBigThreads>(mine, t.red, &wtot);
+      const long long sbase = __shfl_sync(kFull, g, lane & ~1);
+      if ((tid & 1) == 0) sup[tid >> 1] = static_cast<uint32_t>(g);
+      int run = static_cast<int>(g - sbase);
+      for (int i = 0; i < kBigWordsPerThread; ++i) {
+        const int w = w0 + i;
+        pre[pre_idx(w)] = static_cast<uint16_t>(run);
+        run += __popc(bm[bm_idx(w)]);
+      }
+      __syncthreads();
+      for (int w = tid; w < kBigWords; w += kBigThreads) {
+        uint32_t m = bm[bm_idx(w)];
+        if (m) {
+          int64_t pos = woff + sup[w / kBigSuper] + pre[pre_idx(w)];
+          do {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+            ccol[base + pos] = c0 + w * 32 + b;
+            ++pos;
+          } while (m);
+        }
+      }
+      double* crow = cval + base + woff;
+      for (int64_t e = tid; e < wtot; e += kBigThreads) crow[e] = 0.0;
+      __syncthreads();  // rank directory + zeroed C.val visible to the block
+      // ---- pass B (ordered): warp `warp` owns column panel `warp`
+      const int32_t* pcol = poff + warp;
+      for (int64_t e0 = a0; e0 < a1; e0 += 32) {
+        const int64_t j = e0 + lane;
+        int32_t s = 0;
+        int len = 0;
+        double av = 0.0;
+        if (j < a1) {
+          const int64_t k = A.col[j];
+          s = pcol[k * (kPanels + 1)];
+          len = pcol[k * (kPanels + 1) + 1] - s;
+          av = A.val[j];
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int tot = __shfl_sync(kFull, incl, 31);
+        for (int q0 = 0; q0 < tot; q0 += 32) {
+          const int q = q0 + lane;
+          // entry of product q: the first lane whose inclusive prefix exceeds q
+          int ei = 0;
+#pragma unroll
+          for (int b = 16; b > 0; b >>= 1) {
+            const int tv = __shfl_sync(kFull, incl, ei + b - 1);
+            if (tv <= q) ei += b;
+          }
+          const bool valid = q < tot;
+          const int sj = __shfl_sync(kFull, s, ei);
+          const int ej = __shfl_sync(kFull, incl, ei) - __shfl_sync(kFull, len, ei);
+          const double aj = __shfl_sync(kFull, av, ei);
+          int32_t col = 0;
+          double x = 0.0;
+          if (valid) {
+            const int32_t at = sj + (q - ej);
+            col = B.col[at];
+            x = __dmul_rn(aj, B.val[at]);
+          }
+          const uint32_t off = static_cast<uint32_t>(col - c0);
+          const bool in = valid && off < static_cast<uint32_t>(kBigWindow);
+          uint32_t r = 0;
+          if (in) {
+            const uint32_t w = off >> 5;
+            r = sup[w / kBigSuper] + pre[pre_idx(w)] + __popc(bm[bm_idx(w)] & ((1u << (off & 31u)) - 1u));
+          }
+          // several entries in this round: equal columns fold in lane (= A) order
+          const int e_first = __shfl_sync(kFull, ei, 0);
+          if (!__any_sync(kFull, valid && ei != e_first)) {
+            if (in) crow[r] = __dadd_rn(crow[r], x);
+          } else {
+            const unsigned m = __match_any_sync(kFull, in ? static_cast<int>(r) : -1 - lane);
+            const int pos = __popc(m & lt);
+            const int cnt = __popc(m);
+            const int maxc = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt)));
+            const int prev = 31 - __clz(m & lt);  // the group's previous lane (pos > 0)
+            double acc = 0.0;
+            if (in && pos == 0) acc = __dadd_rn(crow[r], x);
+            for (int st = 1; st < maxc; ++st) {
+              const double pv = __shfl_sync(kFull, acc, prev & 31);
+              if (in && pos == st) acc = __dadd_rn(pv, x);
+            }
+            if (in && pos == cnt - 1) crow[r] = acc;
+          }
+          __syncwarp();
+        }
+      }
+      woff += wtot;
+      __syncthreads();
+    }
+    if (tid == 0 && woff != n) atomicOr(&info->error, kErrNumericCount);
+    __syncthreads();
+  }
+}
+
 }  // namespace spgemm_b200

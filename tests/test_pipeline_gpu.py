@@ -177,13 +177,20 @@ def test_spill_to_global_tier(sg, oracle):  # :285-296
     assert out.c.row_nnz(0) == 20000
 
 
-@pytest.mark.parametrize("pair", [(20000, 200), (6000, 60)])
-def test_heap_tier_ordered_is_bitwise(sg, oracle, pair):
-    """ordered_heap=True: heap-tier rows fold in the reference's order (bitwise)."""
+@pytest.mark.parametrize("pair", [(20000, 200), (6000, 60), (3000, 30)])
+@pytest.mark.parametrize("num", ["num_1x", "num_2x", "num_3x"])
+def test_heap_tier_deterministic_is_bitwise(sg, oracle, pair, num):
+    """deterministic=True (default): heap-tier rows fold in the reference's order
+    (bitwise) under every numeric preset; deterministic=False within 1e-12."""
     a, b = spill_pair(*pair)
     a, b = S.random_values(a, 5), S.random_values(b, 6)
-    out = sg.multiply(a, b, sg.SpgemmOptions(ordered_heap=True))
-    assert_matches_oracle(out.c, oracle.spgemm(a, b), bitwise=True)
+    exp = oracle.spgemm(a, b)
+    out = sg.multiply(a, b, sg.SpgemmOptions(num_preset=num))
+    assert_matches_oracle(out.c, exp)
+    again = sg.multiply(a, b, sg.SpgemmOptions(num_preset=num))
+    assert bitwise_equal(again.c, out.c.to_host())
+    out = sg.multiply(a, b, sg.SpgemmOptions(num_preset=num, deterministic=False))
+    assert_matches_oracle(out.c, exp, bitwise=False)
 
 
 def test_spill_threshold_stays_fixed(sg):  # :298-303

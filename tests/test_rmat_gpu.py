@@ -66,15 +66,41 @@ def test_rmat16_full_oracle(sg, oracle):
     a = S.random_values(S.rmat(16, 16, seed=16), 1)
     exp = oracle.spgemm(a, a)
     assert (np.diff(exp.rpt) > 4096).any(), "the case must reach the numeric heap tier"
-    out = sg.multiply(a, a)
-    assert_matches_oracle(out.c, exp)  # bitwise outside the heap tier, 1e-12 inside
-    out = sg.multiply(a, a, sg.SpgemmOptions(ordered_heap=True))
-    assert_matches_oracle(out.c, exp, bitwise=True)
+    out = sg.multiply(a, a)  # deterministic (default): bitwise on every row, heap tier included
+    assert_matches_oracle(out.c, exp)
+    out = sg.multiply(a, a, sg.SpgemmOptions(deterministic=False))  # fp64 atomics in the heap tier
+    assert_matches_oracle(out.c, exp, bitwise=False)
+    out = sg.multiply(a, a, sg.SpgemmOptions(deterministic=False, ordered_heap=True))
+    assert_matches_oracle(out.c, exp)
+
+
+def _identical(x, y):
+    return (np.array_equal(x.c.rpt, y.c.rpt) and np.array_equal(x.c.col, y.c.col)
+            and np.array_equal(x.c.val.view(np.int64), y.c.val.view(np.int64)))
+
+
+def test_rmat16_deterministic_repeat_and_presets(sg, oracle):
+    """test_pipeline.cpp:211-224 and :253-268 (acceptance criterion 3) on a skewed
+    matrix whose rows reach every numeric tier, the heap tier included: repeated
+    runs and all 12 preset combinations give bitwise-identical C, equal to the
+    reference's (num_3x moves rows of 2731..4096 nnz into its bin 7)."""
+    a = S.random_values(S.rmat(16, 16, seed=16), 3)
+    exp = oracle.spgemm(a, a)
+    lens = np.diff(exp.rpt)
+    assert (lens > 4096).any() and ((lens > 2730) & (lens <= 4096)).any()
+    base = sg.multiply(a, a)
+    assert_matches_oracle(base.c, exp)
+    for _ in range(3):
+        assert _identical(sg.multiply(a, a), base)
+    for sym in sg.preset_names(sg.SYMBOLIC):
+        for num in sg.preset_names(sg.NUMERIC):
+            out = sg.multiply(a, a, sg.SpgemmOptions(sym_preset=sym, num_preset=num))
+            assert _identical(out, base), (sym, num)
 
 
 @pytest.mark.slow
 def test_rmat18_sampled(sg, oracle):
-    a = S.rmat(18, 16, seed=18)
+    a = S.random_values(S.rmat(18, 16, seed=18), 7)
     out = _check_sampled(sg, oracle, a, 18)
     assert out.spilled_rows > 0
 
