@@ -228,6 +228,11 @@ __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 #endif
 }
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_add_keep(double* p, double v, uint64_t pol) {
 #ifdef SPGEMM_ABLATE_NOKEEP
   atomicAdd(p, v);
@@ -429,7 +434,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   BigTile& t = *reinterpret_cast<BigTile*>(smem_raw + sizeof(uint32_t) * kBigWordsPad +
                                            sizeof(uint16_t) * kBigPrePad + sizeof(uint32_t) * (kBigWords / kBigSuper));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t keep = l2_evict_last_policy();  // the rows' C.val stays in L2 between its RMWs
   for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
     const int64_t row = rl.row(idx);
     const int64_t base = rpt[row];
@@ -476,9 +481,11 @@ __global__ void __launch_bounds__(kBigThreads, 1)
         }
       }
       double* crow = cval + base + woff;
-      for (int64_t e = tid; e < wtot; e += kBigThreads) crow[e] = 0.0;
+      for (int64_t e = tid; e < wtot; e += kBigThreads) st_keep(crow + e, 0.0, keep);
       __syncthreads();  // rank directory + zeroed C.val visible to the block
-      // ---- pass B (ordered): warp `warp` owns column panel `warp`
+      // ---- pass B (ordered): warp `warp` owns column panel `warp`. One A
+      // entry at a time (its slice's columns are distinct, so the lanes never
+      // share a rank); up to U rounds of one entry are in flight at once.
       const int32_t* pcol = poff + warp;
       for (int64_t e0 = a0; e0 < a1; e0 += 32) {
         const int64_t j = e0 + lane;
@@ -491,59 +498,44 @@ __global__ void __launch_bounds__(kBigThreads, 1)
           len = pcol[k * (kPanels + 1) + 1] - s;
           av = A.val[j];
         }
-        int incl = len;
+        unsigned todo = __ballot_sync(kFull, len > 0);
+        while (todo) {
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1u;
+          const int32_t sj = __shfl_sync(kFull, s, src);
+          const int lj = __shfl_sync(kFull, len, src);
+          const double aj = __shfl_sync(kFull, av, src);
+          constexpr int U = 4;
+          for (int qb = 0; qb < lj; qb += 32 * U) {
+            uint32_t r[U];
+            double x[U];
+            bool in[U];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(kFull, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int tot = __shfl_sync(kFull, incl, 31);
-        for (int q0 = 0; q0 < tot; q0 += 32) {
-          const int q = q0 + lane;
-          // entry of product q: the first lane whose inclusive prefix exceeds q
-          int ei = 0;
-#pragma unroll
-          for (int b = 16; b > 0; b >>= 1) {
-            const int tv = __shfl_sync(kFull, incl, ei + b - 1);
-            if (tv <= q) ei += b;
-          }
-          const bool valid = q < tot;
-          const int sj = __shfl_sync(kFull, s, ei);
-          const int ej = __shfl_sync(kFull, incl, ei) - __shfl_sync(kFull, len, ei);
-          const double aj = __shfl_sync(kFull, av, ei);
-          int32_t col = 0;
-          double x = 0.0;
-          if (valid) {
-            const int32_t at = sj + (q - ej);
-            col = B.col[at];
-            x = __dmul_rn(aj, B.val[at]);
-          }
-          const uint32_t off = static_cast<uint32_t>(col - c0);
-          const bool in = valid && off < static_cast<uint32_t>(kBigWindow);
-          uint32_t r = 0;
-          if (in) {
-            const uint32_t w = off >> 5;
-            r = sup[w / kBigSuper] + pre[pre_idx(w)] + __popc(bm[bm_idx(w)] & ((1u << (off & 31u)) - 1u));
-          }
-          // several entries in this round: equal columns fold in lane (= A) order
-          const int e_first = __shfl_sync(kFull, ei, 0);
-          if (!__any_sync(kFull, valid && ei != e_first)) {
-            if (in) crow[r] = __dadd_rn(crow[r], x);
-          } else {
-            const unsigned m = __match_any_sync(kFull, in ? static_cast<int>(r) : -1 - lane);
-            const int pos = __popc(m & lt);
-            const int cnt = __popc(m);
-            const int maxc = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(cnt)));
-            const int prev = 31 - __clz(m & lt);  // the group's previous lane (pos > 0)
-            double acc = 0.0;
-            if (in && pos == 0) acc = __dadd_rn(crow[r], x);
-            for (int st = 1; st < maxc; ++st) {
-              const double pv = __shfl_sync(kFull, acc, prev & 31);
-              if (in && pos == st) acc = __dadd_rn(pv, x);
+            for (int u = 0; u < U; ++u) {
+              const int q = qb + 32 * u + lane;
+              int32_t col = 0;
+              double bv = 0.0;
+              if (q < lj) {
+                col = B.col[sj + q];
+                bv = B.val[sj + q];
+              }
+              const uint32_t off = static_cast<uint32_t>(col - c0);
+              in[u] = q < lj && off < static_cast<uint32_t>(kBigWindow);
+              x[u] = __dmul_rn(aj, bv);
+              r[u] = 0;
+              if (in[u]) {
+                const uint32_t w = off >> 5;
+                r[u] = sup[w / kBigSuper] + pre[pre_idx(w)] + __popc(bm[bm_idx(w)] & ((1u << (off & 31u)) - 1u));
+              }
             }
-            if (in && pos == cnt - 1) crow[r] = acc;
+            double cur[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) cur[u] = in[u] ? ld_keep(crow + r[u], keep) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (in[u]) st_keep(crow + r[u], __dadd_rn(cur[u], x[u]), keep);
           }
-          __syncwarp();
+          __syncwarp();  // this entry's updates before the next entry's
         }
       }
       woff += wtot;
