@@ -113,7 +113,7 @@ class ClockSampler:
 def cpu_baseline(a, rows_frac=1.0, runs=2):
     """The reference CPU pipeline (oracle/_ref, all host threads) on a bounded sample."""
     from oracle import oracle as O
-    from paper_2206_07244_b200.api import CsrMatrix
+    CsrMatrix = type(a)
     m = a.to_host()
     if rows_frac < 1.0:
         r0 = int(m.rows * (0.5 - rows_frac / 2))
@@ -132,7 +132,8 @@ def cpu_baseline(a, rows_frac=1.0, runs=2):
             _, info = O.ref_multiply(sample, m)
             ts.append(time.perf_counter() - t0)
         t = sum(ts) / len(ts)
-        return {"value": 2 * info["total_nprod"] / t / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+        return {"value": 2 * info["total_nprod"] / t / 1e9, "unit": UNIT, "cores": info["workers"] or cores,
+                "kind": "reference", "cpu": cpu_model(), "host_threads": cores,
                 "sample": f"oracle/_ref spgemm::multiply (workers={info['workers']}) on {desc}, "
                           f"1 warm-up + {runs} timed, mean {t:.3f} s"}
     # C restatement (single thread) on a smaller sample
@@ -157,60 +158,129 @@ def stencil_weak(n_ranks):
     return S._stencil((128, 128, 128 * n_ranks), offs, 26.0, -1.0)
 
 
+def launch_bytes(sg, torch, a, b, device, device_tensors):
+    """Algorithmic bytes of one product C = A*B (A + B + C, each
+    8*(rows+1) + 12*nnz) and their split over the per-bin launches: a launch
+    for symbolic bin j (tag "s<j>") or numeric bin j ("n<j>") is charged its
+    rows' A bytes, their C bytes (numeric, and the speculative numeric of the
+    symbolic phase) or their 8-byte counts (symbolic), plus B's bytes times the
+    rows' share of the product's nprod (B is gathered per product)."""
+    import numpy as np
+    nprod, total = sg.compute_nprod(a, b, device=device)
+    dm, out = sg.multiply_device(a, b, device=device)
+    crpt = torch.as_tensor(device_tensors(dm)[0]).cpu().numpy() if dm.rows >= 0 else None
+    dm.free()
+    arpt = a.rpt.cpu().numpy() if hasattr(a.rpt, "cpu") else np.asarray(a.rpt)
+    nnza = np.diff(arpt)
+    nnzc = np.diff(crpt)
+    bbytes = csr_bytes(b.rows, b.nnz())
+    step = csr_bytes(a.rows, int(nnza.sum())) + bbytes + csr_bytes(a.rows, int(nnzc.sum()))
+    sym = np.asarray(sg.symbolic_preset("sym_1.2x").upper[:-1])
+    num = np.asarray(sg.numeric_preset("num_2x").upper[:-1])
+    sbin = np.searchsorted(sym, nprod, side="left")
+    nbin = np.searchsorted(num, nnzc, side="left")
+    share = nprod.astype(np.float64) / max(total, 1) * bbytes
+    out_b = {}
+    for j in range(8):
+        m = sbin == j
+        if m.any():
+            base = float((16 + 12 * nnza[m]).sum() + share[m].sum())
+            out_b[f"s{j}"] = base + 8.0 * int(m.sum())                       # symbolic: the row counts
+            out_b[f"s{j}+c"] = base + float((16 + 12 * nnzc[m]).sum())      # speculative numeric: C rows
+        m = nbin == j
+        if m.any():
+            out_b[f"n{j}"] = float((16 + 12 * nnza[m]).sum() + share[m].sum() + (16 + 12 * nnzc[m]).sum())
+    return step, out_b
+
+
 # ---------------------------------------------------------------- main
+def cpu_model() -> str:
+    """The host CPU (state the core count and CPU model)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_synthetic():
+    """paper_2206_07244_b200/synthetic.py loaded by file path: the reference arm
+    builds the same matrices without importing the package (so the sm_100a
+    library is never loaded into its process)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_spgemm_synthetic_host",
+                                                  os.path.join(ROOT, "paper_2206_07244_b200", "synthetic.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def run_reference(args):
+    """The reference's own CPU pipeline (oracle/_ref: the unmodified proj/core
+    compiled in place) through its public spgemm::multiply, with every host
+    thread, on this arm's workload: the full product for configs 1, 2 and 4 (4 =
+    A*P then R*(AP), both on the host), a bounded row sample for configs 3 and 5,
+    whose C does not fit host memory."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2206_07244_b200.api import CsrMatrix
+    S = host_synthetic()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     workload = CONFIG_NAMES[args.config]
     if args.config == 5:
-        from paper_2206_07244_b200 import synthetic as S
         mats = [S.rmat(args.rmat_scale, 16, seed=args.rmat_scale)] * 2
-    elif world > 1 and args.config == 2:
-        # the b200 arm's N-GPU workload (weak scaling): sampled the same way
-        g = stencil_weak(world)
-        mats = [g, g]
-        workload = f"C=A*A 3D 27-pt stencil 128x128x{128 * world} (weak: 128^3 rows/GPU), nprod-balanced row blocks"
     else:
-        mats = build_workload(args.config)
+        mats = list(S.config_matrices(args.config))
     a = mats[0]
-    frac = {1: 1.0, 2: 0.25, 3: 0.02, 4: 1.0, 5: 0.0005}[args.config]
-    if args.config == 2 and world > 1:
-        frac /= world  # same sample size as at N=1 (the weak-scaled matrix is N x larger)
+    frac = {1: 1.0, 2: 1.0, 3: 0.02, 4: 1.0, 5: 0.0005}[args.config]
     r0 = int(a.rows * (0.5 - frac / 2)) if frac < 1 else 0
     r1 = r0 + int(a.rows * frac) if frac < 1 else a.rows
-    rpt = a.rpt[r0:r1 + 1] - a.rpt[r0]
-    sample = CsrMatrix(r1 - r0, a.cols, rpt, a.col[a.rpt[r0]:a.rpt[r1]], a.val[a.rpt[r0]:a.rpt[r1]])
-    b = mats[1]
-    kind = "reference" if O.ref_available() else "port"
+    if frac < 1:
+        rpt = a.rpt[r0:r1 + 1] - a.rpt[r0]
+        sample = S.CsrMatrix(r1 - r0, a.cols, rpt, a.col[a.rpt[r0]:a.rpt[r1]], a.val[a.rpt[r0]:a.rpt[r1]])
+        desc = f"rows [{r0},{r1}) of A times B (C does not fit host memory)"
+    else:
+        sample = a
+        desc = "the full product" + (" chain A*P then R*(AP)" if args.config == 4 else "")
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
 
     def step():
-        if kind == "reference":
-            _, info = O.ref_multiply(sample, b)
-            return info["total_nprod"]
-        O.spgemm(sample, b)
-        return O.compute_nprod(sample, b)[1]
+        if args.config == 4:
+            _, p, r = mats
+            ap, i1 = O.ref_multiply(a, p)
+            _, i2 = O.ref_multiply(r, ap)
+            return i1["total_nprod"] + i2["total_nprod"], i1["workers"]
+        _, info = O.ref_multiply(sample, mats[1])
+        return info["total_nprod"], info["workers"]
 
     for _ in range(args.warmup):
         step()
     t0 = time.perf_counter()
     nprod = 0
+    workers = 0
     for _ in range(args.steps):
-        nprod += step()
+        n, workers = step()
+        nprod += n
     t = time.perf_counter() - t0
     value = 2 * nprod / t / 1e9
-    cores = os.cpu_count() or 1 if kind == "reference" else 1
+    cores = os.cpu_count() or 1
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload, "sample_rows": [r0, r1]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"rows [{r0},{r1}) of config {args.config}'s A times B per step"},
+        "config": {"workload": workload, "nprod_per_step": nprod // args.steps,
+                   **({"sample_rows": [r0, r1]} if frac < 1 else {})},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers or cores, "kind": "reference",
+                         "cpu": cpu_model(), "host_threads": cores,
+                         "sample": f"oracle/_ref spgemm::multiply (workers={workers}) on {desc}, "
+                                   f"{args.warmup} warm-up + {args.steps} timed steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -402,49 +472,51 @@ def main():
     roof = None
     step_roof = None
     if rank == 0 and kernels:
-        top = max(kernels.items(), key=lambda kv: kv[1][1])
-        name, (n_launch, ms_total) = top
+        # the dominant launch record: "<kernel>#s<bin>" / "#n<bin>" (phase, bin)
+        name, (n_launch, ms_total) = max(kernels.items(), key=lambda kv: kv[1][1])
         avg_s = ms_total / n_launch * 1e-3
-        # C bytes from the last step's report
-        if pairs is not None:
-            a, b = pairs[0]
-            dm, out = sg.multiply_device(a, b, device=local)
-            c_nnz, c_rows = out.stats.nnz_of_product, a.rows
-            dm.free()
-            ab = csr_bytes(a.rows, a.nnz()) + csr_bytes(b.rows, b.nnz())
-            step_bytes = ab + csr_bytes(c_rows, c_nnz)
+        prods = pairs if pairs is not None else [(dev[0], dev[1]), None]
+        tag_bytes = {}   # per step, summed over the step's products
+        step_bytes = 0
+        for pr in prods:
+            if pr is None:  # RAP: R * (AP), AP from the chain's first product
+                a, p, r = dev
+                dm1, _ = sg.multiply_device(a, p, device=local)
+                pr = (r, CsrMatrix(dm1.rows, dm1.cols, *device_tensors(dm1)))
+                b_keep = dm1
+            else:
+                b_keep = None
+            sb, tb = launch_bytes(sg, torch, pr[0], pr[1], local, device_tensors)
+            step_bytes += sb
+            for k, v in tb.items():
+                tag_bytes[k] = tag_bytes.get(k, 0) + v
+            if b_keep is not None:
+                b_keep.free()
+        tag = name.rsplit("#", 1)[1] if "#" in name else None
+        if tag and tag[0] == "s" and "spec" in name:
+            tag += "+c"
+        launches_per_step = max(1, n_launch // args.steps)
+        if tag in tag_bytes:
+            kernel_bytes = tag_bytes[tag] / launches_per_step
+            attribution = (f"rows of {'symbolic' if tag[0] == 's' else 'numeric'} bin {tag[1:2]}: their A rows"
+                           f"{' and C rows' if tag[0] == 'n' or 'spec' in name else ' and counts'}, plus B's "
+                           f"bytes times the rows' share of nprod")
         else:
-            a, p, r = dev
-            dm1, o1 = sg.multiply_device(a, p, device=local)
-            ap_b = csr_bytes(dm1.rows, dm1.nnz)
-            dm1.free()
-            rap_nnz = 6_859_000 if args.config == 4 else 0
-            step_bytes = (csr_bytes(a.rows, a.nnz()) + csr_bytes(p.rows, p.nnz()) + ap_b +
-                          csr_bytes(r.rows, r.nnz()) + ap_b + csr_bytes(r.rows, rap_nnz))
-        # per-kernel algorithmic bytes: the dominant kernel is a numeric-phase
-        # kernel reading A (rpt, col, val), B and C.rpt and writing C.col/C.val;
-        # a launch that handles a fraction of the rows gets that fraction.
-        frac = 1.0
-        if name.startswith("k_num") or name.startswith("k_sym"):
-            frac = 1.0 / max(1, n_launch // args.steps)
-        kernel_bytes = step_bytes * frac if name.startswith("k_num") else None
-        if name.startswith("k_sym") and pairs is not None:
-            a, b = pairs[0]
-            kernel_bytes = frac * (8 * (a.rows + 1) + 4 * a.nnz() + 8 * (b.rows + 1) + 4 * b.nnz() + 8 * a.rows)
-        if kernel_bytes is None:
             kernel_bytes = step_bytes
+            attribution = "whole step (kernel not bound to a bin)"
         achieved = kernel_bytes / avg_s / 1e9
         traffic = None
         prof_path = os.path.join(ROOT, "profiles", f"ncu_config{args.config}_summary.json")
         if os.path.exists(prof_path):
             with open(prof_path) as f:
                 prof = json.load(f)
-            k = prof.get("kernels", {}).get(name)
+            k = prof.get("kernels", {}).get(name.split("#")[0])
             if k:
                 traffic = k.get("dram_bytes_per_launch")
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                "algorithmic_bytes_per_launch": kernel_bytes, "avg_launch_ms": avg_s * 1e3,
+                "algorithmic_bytes_per_launch": kernel_bytes, "bytes_attribution": attribution,
+                "avg_launch_ms": avg_s * 1e3,
                 "share_of_step": ms_total / t_prof_ms, "profiled_pass_ms_per_step": t_prof_ms / args.steps,
                 "profiled_pass": "second timed pass with per-launch events; bins serialised on one stream so each launch is timed alone"}
         step_roof = {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,

@@ -202,6 +202,7 @@ struct spgemm_ctx {
     cudaEvent_t a, b;
   };
   std::vector<ProfRec> prof_recs;
+  std::string prof_tag;  // appended to the names of per-bin launches while profiling
   std::vector<cudaEvent_t> ev_pool;
   // Per-call scratch (the metadata arena, staged host inputs) kept across
   // multiplies: re-allocating multi-GB arenas every call fragments the
@@ -287,6 +288,7 @@ struct LaunchScope {
   cudaEvent_t a = nullptr;
   LaunchScope(spgemm_ctx* c, std::string n, cudaStream_t st) : ctx(c), name(std::move(n)), s(st) {
     if (ctx->prof) {
+      name += ctx->prof_tag;  // "#s<bin>" / "#n<bin>": the phase and bin of a per-bin launch
       a = pooled_event(ctx);
       ck(cudaEventRecord(a, s), "prof event");
     }
@@ -613,6 +615,11 @@ void spgemm_pipeline::symbolic_binning() {
   (idx32 ? &k_num_group<G, T, E, N, int32_t, false> : &k_num_group<G, T, E, N, int64_t, false>)
 
 void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s) {
+  ctx->prof_tag = "#s" + std::to_string(bin);
+  struct Untag {
+    spgemm_ctx* c;
+    ~Untag() { c->prof_tag.clear(); }
+  } untag{ctx};
   const int64_t u = sym_plan.config.upper[bin];
   const bool g8 = avg_b_len <= kG8MaxBLen;
   auto group = [&](auto kern, int G, int T, int NGRP, int WB) {
@@ -809,6 +816,11 @@ int64_t spgemm_pipeline::finalize_rpt(bool host_total) {
 void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s, int32_t* gkeys,
                                      double* gvals, uint32_t* gbits, int64_t gslots,
                                      int64_t gwords, int gblocks) {
+  ctx->prof_tag = "#n" + std::to_string(bin);
+  struct Untag {
+    spgemm_ctx* c;
+    ~Untag() { c->prof_tag.clear(); }
+  } untag{ctx};
   const int64_t u = num_plan.config.upper[bin];
   const bool g8 = avg_b_len <= kG8MaxBLen;
   auto group = [&](auto kern, int G, int T, int E, int NGRP) {

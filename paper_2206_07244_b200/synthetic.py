@@ -16,7 +16,28 @@ from __future__ import annotations
 
 import numpy as np
 
-from .api import CsrMatrix, InvalidArgument
+try:
+    from .api import CsrMatrix, InvalidArgument
+except ImportError:
+    # Loaded by file path, outside the package (bench.py --impl reference builds
+    # the reference arm's inputs this way): no package import, so the sm_100a
+    # library is never loaded into the reference's process. A host-only record
+    # with the fields the checkers and the reference binding read.
+    class InvalidArgument(ValueError):
+        pass
+
+    class CsrMatrix:  # noqa: D101 -- host arrays only
+        def __init__(self, rows, cols, rpt, col, val):
+            self.rows, self.cols = int(rows), int(cols)
+            self.rpt = np.ascontiguousarray(rpt, np.int64)
+            self.col = np.ascontiguousarray(col, np.int32)
+            self.val = np.ascontiguousarray(val, np.float64)
+
+        def to_host(self):
+            return self
+
+        def nnz(self) -> int:
+            return int(self.rpt[self.rows]) if self.rows >= 0 else 0
 
 
 def identity_csr(n: int) -> CsrMatrix:
