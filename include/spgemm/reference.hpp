@@ -1,8 +1,10 @@
-// spgemm/reference.hpp -- statistics types of the reference (reference.hpp:1-36).
-// reference_spgemm / compute_nprod / compression_ratio / input_stats are the
-// reference's CPU oracle functions; this library does not implement them (it
-// ships no CPU SpGEMM). Tests link them from the reference sources (oracle role);
-// the device nprod kernel is exposed as spgemm_compute_nprod in spgemm_capi.h.
+// spgemm/reference.hpp -- the reference's statistics and oracle entry points
+// (reference.hpp:1-36), defined by libspgemm_b200 (cxx_api.cpp):
+//   compute_nprod      kernel K1 on the device (spgemm_compute_nprod)
+//   compression_ratio  nprod / nnz; std::domain_error when nnz <= 0
+//   input_stats        host scan of the row pointers
+//   reference_spgemm   the device product with default (deterministic)
+//                      options: bitwise the reference's row-by-row oracle
 #pragma once
 
 #include <span>

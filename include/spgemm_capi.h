@@ -200,6 +200,16 @@ void spgemm_matrix_device_ptrs(const spgemm_matrix* m, const int64_t** rpt, cons
 spgemm_status spgemm_matrix_download(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t* rpt,
                                      int32_t* col, double* val);
 void spgemm_matrix_free(spgemm_matrix* m);
+/* B200 extension: device-resident chaining (the reference's --b / RAP chain,
+ * spgemm_bench_main.cpp:84, 130-135, without the host round trip). Fills a
+ * device view (on_device = 1) of C that can be passed straight back as an
+ * operand of spgemm_multiply / spgemm_pipeline_create. The view borrows C's
+ * buffers: valid until spgemm_matrix_free or a releasing download. */
+spgemm_status spgemm_matrix_as_operand(const spgemm_matrix* m, spgemm_csr_view* out);
+/* Orders the context's next work after everything queued so far on `stream`
+ * (a cudaStream_t; NULL = the legacy default stream), so device operands a
+ * producer wrote on its own stream are complete before K1 reads them. */
+spgemm_status spgemm_ctx_wait_stream(spgemm_ctx* ctx, void* stream);
 /* B200 extension: stream-ordered D2H of C on the context's copy lane. Returns
  * at once; the copy starts when the work already queued on the context's
  * stream (the product) is done, so it overlaps the NEXT product's H2D and

@@ -222,6 +222,8 @@ class CsrMatrix:
 
     def _view(self) -> _c.CsrView:
         if self.on_device:
+            if self.rpt.numel() != self.rows + 1:
+                raise InvalidArgument("rpt length is not rows+1")
             return _c.CsrView(self.rows, self.cols, self.rpt.data_ptr(), self.col.data_ptr() or None,
                               self.val.data_ptr() or None, 1)
         if self.rpt.size != self.rows + 1:
@@ -434,6 +436,8 @@ def compute_nprod(a: CsrMatrix, b: CsrMatrix, out: Optional[np.ndarray] = None, 
         raise InvalidArgument("compute_nprod: out length != a.rows")
     total = C.c_int64()
     va, vb = a._view(), b._view()
+    if a.on_device or b.on_device:
+        _order_device_operands(get_context(device), a, b)
     _check(_c.lib.spgemm_compute_nprod(get_context(device).handle, C.byref(va), C.byref(vb), out.ctypes.data,
                                        C.byref(total)))
     return out, int(total.value)
@@ -583,6 +587,28 @@ class DeviceMatrix:
                                              C.byref(v), C.byref(h)))
         return v.value, h.value
 
+    def as_operand(self) -> CsrMatrix:
+        """C as a device-resident operand of the next product (zero copy; the
+        reference's chained --b / RAP flow without the host round trip). The
+        returned CsrMatrix keeps this DeviceMatrix alive; its tensors are valid
+        until :meth:`free`."""
+        import torch
+        v = _c.CsrView()
+        _check(_c.lib.spgemm_matrix_as_operand(self.handle, C.byref(v)))
+        dev = torch.device("cuda", self.ctx.device)
+
+        def wrap(ptr, n, typestr, dtype):
+            if n == 0 or not ptr:
+                return torch.zeros(0, dtype=dtype, device=dev)
+            cai = type("_Cai", (), {"__cuda_array_interface__": {"shape": (n,), "typestr": typestr,
+                                                                  "data": (ptr, False), "version": 3}})()
+            return torch.as_tensor(cai, device=dev)
+
+        m = CsrMatrix(self.rows, self.cols, wrap(v.rpt, self.rows + 1, "<i8", torch.int64),
+                      wrap(v.col, self.nnz, "<i4", torch.int32), wrap(v.val, self.nnz, "<f8", torch.float64))
+        m._owner = self  # the buffers belong to this DeviceMatrix
+        return m
+
     def download(self) -> CsrMatrix:
         rpt = np.empty(self.rows + 1, np.int64)
         col = np.empty(self.nnz, np.int32)
@@ -602,6 +628,21 @@ class DeviceMatrix:
             pass
 
 
+def _order_device_operands(ctx: "Context", *ms: CsrMatrix) -> None:
+    """Device operands must live on the context's device, and the product is
+    ordered after the work torch has queued on its current stream there (the
+    producer of the tensors): an event on that stream, waited on by the
+    context's stream -- no host synchronisation."""
+    import torch
+    for m in ms:
+        if m.on_device:
+            for t in (m.rpt, m.col, m.val):
+                if t.device.index != ctx.device:
+                    raise InvalidArgument(f"device operand on cuda:{t.device.index}, context on cuda:{ctx.device}")
+    stream = torch.cuda.current_stream(ctx.device)
+    _check(_c.lib.spgemm_ctx_wait_stream(ctx.handle, C.c_void_p(stream.cuda_stream or None)))
+
+
 class SpgemmPipeline:
     """pipeline.hpp:119-168: six-step two-phase SpGEMM, drivable one step at a time."""
 
@@ -613,6 +654,8 @@ class SpgemmPipeline:
         self._rows = a.rows
         self._cols = b.cols
         self._va, self._vb = a._view(), b._view()
+        if a.on_device or b.on_device:
+            _order_device_operands(self._ctx, a, b)
         if (not a.on_device and not b.on_device and a is not b and a.rpt is b.rpt):
             self._vb = self._va
         h = C.c_void_p()

@@ -1384,6 +1384,30 @@ void spgemm_matrix_device_ptrs(const spgemm_matrix* m, const int64_t** rpt, cons
   *val = m->val;
 }
 
+spgemm_status spgemm_matrix_as_operand(const spgemm_matrix* m, spgemm_csr_view* out) {
+  return guard([&] {
+    if (!m || !out) fail(SPGEMM_INVALID_ARGUMENT, "spgemm_matrix_as_operand: null argument");
+    if (!m->rpt) fail(SPGEMM_INVALID_ARGUMENT, "spgemm_matrix_as_operand: C's buffers were released");
+    out->rows = m->rows;
+    out->cols = m->cols;
+    out->rpt = m->rpt;
+    out->col = m->col;
+    out->val = m->val;
+    out->on_device = 1;
+  });
+}
+
+spgemm_status spgemm_ctx_wait_stream(spgemm_ctx* ctx, void* stream) {
+  return guard([&] {
+    if (!ctx) fail(SPGEMM_INVALID_ARGUMENT, "spgemm_ctx_wait_stream: null context");
+    DeviceGuard g(ctx->device);
+    cudaEvent_t e = pooled_event(ctx);
+    ck(cudaEventRecord(e, stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy), "record producer stream");
+    ck(cudaStreamWaitEvent(ctx->main_s, e, 0), "context waits for producer stream");
+    ctx->ev_pool.push_back(e);
+  });
+}
+
 spgemm_status spgemm_matrix_download(spgemm_ctx* ctx, const spgemm_matrix* m, int64_t* rpt,
                                      int32_t* col, double* val) {
   return guard([&] {

@@ -18,6 +18,7 @@
 #include "spgemm/binning.hpp"
 #include "spgemm/csr.hpp"
 #include "spgemm/pipeline.hpp"
+#include "spgemm/reference.hpp"
 #include "spgemm_capi.h"
 
 namespace spgemm {
@@ -133,102 +134,119 @@ ExecutionPlan from_c(const spgemm_plan& p) {
 }  // namespace
 
 // ------------------------------------------------------------------- csr
-CsrMatrix csr_from_coo(const CooEntries& coo) {
+// Host container utilities (csr.hpp). Semantics follow the reference
+// (csr.cpp:12-181): the exception types and messages are part of the
+// interface its tests check; the implementations are this library's own.
+namespace {
+
+void check_coo_shape(const CooEntries& coo) {
   if (coo.rows < 0 || coo.cols < 0) throw std::out_of_range("csr_from_coo: negative matrix shape");
   if (coo.cols > std::numeric_limits<index_t>::max())
     throw std::out_of_range("csr_from_coo: column count exceeds 32-bit index range");
-  for (const CooEntry& e : coo.entries) {
-    if (e.row < 0 || e.row >= coo.rows || e.col < 0 || e.col >= coo.cols) {
-      std::ostringstream os;
-      os << "csr_from_coo: entry (" << e.row << ", " << e.col << ") outside " << coo.rows << "x" << coo.cols
-         << " shape";
-      throw std::out_of_range(os.str());
-    }
-  }
-  // bucket by row keeping input order, stable-sort each row by column, fold
-  // duplicates left to right
-  std::vector<offset_t> start(static_cast<std::size_t>(coo.rows) + 1, 0);
-  for (const CooEntry& e : coo.entries) ++start[static_cast<std::size_t>(e.row) + 1];
-  std::partial_sum(start.begin(), start.end(), start.begin());
-  std::vector<std::pair<index_t, double>> rowed(coo.entries.size());
-  std::vector<offset_t> fill(start.begin(), start.end() - 1);
-  for (const CooEntry& e : coo.entries)
-    rowed[static_cast<std::size_t>(fill[static_cast<std::size_t>(e.row)]++)] = {static_cast<index_t>(e.col), e.value};
+  const auto outside = std::find_if(coo.entries.begin(), coo.entries.end(), [&](const CooEntry& e) {
+    return static_cast<std::uint64_t>(e.row) >= static_cast<std::uint64_t>(coo.rows) ||
+           static_cast<std::uint64_t>(e.col) >= static_cast<std::uint64_t>(coo.cols);
+  });
+  if (outside != coo.entries.end())
+    throw std::out_of_range("csr_from_coo: entry (" + std::to_string(outside->row) + ", " +
+                            std::to_string(outside->col) + ") outside " + std::to_string(coo.rows) + "x" +
+                            std::to_string(coo.cols) + " shape");
+}
+
+}  // namespace
+
+// One global stable order of the triples by (row, column): equal positions keep
+// their file order, so a duplicate run folds left to right in input order.
+CsrMatrix csr_from_coo(const CooEntries& coo) {
+  check_coo_shape(coo);
+  const auto& t = coo.entries;
+  std::vector<std::size_t> order(t.size());
+  std::iota(order.begin(), order.end(), std::size_t{0});
+  std::stable_sort(order.begin(), order.end(), [&t](std::size_t x, std::size_t y) {
+    return t[x].row != t[y].row ? t[x].row < t[y].row : t[x].col < t[y].col;
+  });
   CsrMatrix m;
   m.rows = coo.rows;
   m.cols = coo.cols;
   m.rpt.assign(static_cast<std::size_t>(coo.rows) + 1, 0);
-  m.col.reserve(rowed.size());
-  m.val.reserve(rowed.size());
-  for (std::int64_t i = 0; i < coo.rows; ++i) {
-    auto b = rowed.begin() + start[static_cast<std::size_t>(i)];
-    auto e = rowed.begin() + start[static_cast<std::size_t>(i) + 1];
-    std::stable_sort(b, e, [](const auto& x, const auto& y) { return x.first < y.first; });
-    const std::size_t row_begin = m.col.size();
-    for (auto it = b; it != e; ++it) {
-      if (m.col.size() > row_begin && m.col.back() == it->first) {
-        m.val.back() += it->second;
-      } else {
-        m.col.push_back(it->first);
-        m.val.push_back(it->second);
-      }
+  m.col.reserve(t.size());
+  m.val.reserve(t.size());
+  std::int64_t last_row = -1;
+  std::int64_t last_col = -1;
+  for (const std::size_t idx : order) {
+    const CooEntry& e = t[idx];
+    if (e.row == last_row && e.col == last_col) {
+      m.val.back() += e.value;
+      continue;
     }
-    m.rpt[static_cast<std::size_t>(i) + 1] = static_cast<offset_t>(m.col.size());
+    m.col.push_back(static_cast<index_t>(e.col));
+    m.val.push_back(e.value);
+    ++m.rpt[static_cast<std::size_t>(e.row) + 1];
+    last_row = e.row;
+    last_col = e.col;
   }
+  std::partial_sum(m.rpt.begin(), m.rpt.end(), m.rpt.begin());
   return m;
 }
 
 CooEntries to_coo(const CsrMatrix& m) {
   CooEntries coo{m.rows, m.cols, {}};
-  coo.entries.reserve(static_cast<std::size_t>(m.nnz()));
-  for (std::int64_t i = 0; i < m.rows; ++i)
-    for (offset_t p = m.rpt[static_cast<std::size_t>(i)]; p < m.rpt[static_cast<std::size_t>(i) + 1]; ++p)
-      coo.entries.push_back({i, m.col[static_cast<std::size_t>(p)], m.val[static_cast<std::size_t>(p)]});
+  coo.entries.resize(static_cast<std::size_t>(m.nnz()));
+  std::int64_t row = 0;
+  for (std::size_t p = 0; p < coo.entries.size(); ++p) {
+    while (static_cast<offset_t>(p) >= m.rpt[static_cast<std::size_t>(row) + 1]) ++row;
+    coo.entries[p] = CooEntry{row, m.col[p], m.val[p]};
+  }
   return coo;
 }
 
 std::string ValidationReport::to_string() const {
-  std::ostringstream os;
-  for (const Violation& v : violations) {
-    if (v.row >= 0) os << "row " << v.row << ": ";
-    os << v.message << '\n';
-  }
-  return os.str();
+  std::string text;
+  for (const Violation& v : violations)
+    text += (v.row >= 0 ? "row " + std::to_string(v.row) + ": " : std::string()) + v.message + "\n";
+  return text;
 }
 
 ValidationReport validate_csr(const CsrMatrix& m) {
-  ValidationReport r;
-  auto add = [&r](std::int64_t row, std::string msg) { r.violations.push_back({row, std::move(msg)}); };
+  ValidationReport report;
+  auto& out = report.violations;
   if (m.rows < 0 || m.cols < 0) {
-    add(-1, "negative matrix shape");
-    return r;
+    out.push_back({-1, "negative matrix shape"});
+    return report;
   }
-  if (m.rpt.size() != static_cast<std::size_t>(m.rows) + 1) {
-    add(-1, "rpt length is not rows+1");
-    return r;
+  const auto rows = static_cast<std::size_t>(m.rows);
+  if (m.rpt.size() != rows + 1) {
+    out.push_back({-1, "rpt length is not rows+1"});
+    return report;
   }
-  if (m.rpt[0] != 0) add(-1, "rpt[0] is not 0");
-  for (std::int64_t i = 0; i < m.rows; ++i)
-    if (m.rpt[static_cast<std::size_t>(i) + 1] < m.rpt[static_cast<std::size_t>(i)])
-      add(i, "non-monotone rpt at row " + std::to_string(i));
-  if (m.rpt.back() != static_cast<offset_t>(m.col.size())) add(-1, "rpt[rows] does not equal len(col)");
-  if (m.col.size() != m.val.size()) add(-1, "len(col) does not equal len(val)");
-  const offset_t limit = static_cast<offset_t>(std::min(m.col.size(), m.val.size()));
-  for (std::int64_t i = 0; i < m.rows; ++i) {
-    const offset_t lo = m.rpt[static_cast<std::size_t>(i)], hi = m.rpt[static_cast<std::size_t>(i) + 1];
-    if (lo < 0 || hi > limit || hi < lo) continue;
+  // row pointers
+  if (m.rpt.front() != 0) out.push_back({-1, "rpt[0] is not 0"});
+  for (std::size_t i = 0; i < rows; ++i)
+    if (m.rpt[i + 1] < m.rpt[i])
+      out.push_back({static_cast<std::int64_t>(i), "non-monotone rpt at row " + std::to_string(i)});
+  if (m.rpt.back() != static_cast<offset_t>(m.col.size())) out.push_back({-1, "rpt[rows] does not equal len(col)"});
+  if (m.col.size() != m.val.size()) out.push_back({-1, "len(col) does not equal len(val)"});
+  // columns of every row whose extent is readable (others were reported above)
+  const auto readable = static_cast<offset_t>(std::min(m.col.size(), m.val.size()));
+  for (std::size_t i = 0; i < rows; ++i) {
+    const offset_t lo = m.rpt[i], hi = m.rpt[i + 1];
+    if (lo < 0 || lo > hi || hi > readable) continue;
+    const auto row = static_cast<std::int64_t>(i);
+    index_t prev = -1;
     for (offset_t p = lo; p < hi; ++p) {
       const index_t c = m.col[static_cast<std::size_t>(p)];
-      if (c < 0 || c >= m.cols) add(i, "column index " + std::to_string(c) + " out of range");
-      if (p > lo) {
-        const index_t prev = m.col[static_cast<std::size_t>(p) - 1];
-        if (c == prev) add(i, "duplicate column " + std::to_string(c));
-        else if (c < prev)
-          add(i, "unsorted columns (" + std::to_string(prev) + " before " + std::to_string(c) + ")");
+      if (c < 0 || c >= m.cols) out.push_back({row, "column index " + std::to_string(c) + " out of range"});
+      if (p == lo) {
+        prev = c;
+        continue;
       }
+      if (c == prev) out.push_back({row, "duplicate column " + std::to_string(c)});
+      if (c < prev)
+        out.push_back({row, "unsorted columns (" + std::to_string(prev) + " before " + std::to_string(c) + ")"});
+      prev = c;
     }
   }
-  return r;
+  return report;
 }
 
 std::vector<double> to_dense(const CsrMatrix& m, std::int64_t max_cells) {
@@ -236,22 +254,52 @@ std::vector<double> to_dense(const CsrMatrix& m, std::int64_t max_cells) {
   if (cells > max_cells)
     throw std::length_error("to_dense: matrix exceeds the dense-expansion guard of " + std::to_string(max_cells) +
                             " cells");
-  std::vector<double> d(static_cast<std::size_t>(cells), 0.0);
-  for (std::int64_t i = 0; i < m.rows; ++i)
-    for (offset_t p = m.rpt[static_cast<std::size_t>(i)]; p < m.rpt[static_cast<std::size_t>(i) + 1]; ++p)
-      d[static_cast<std::size_t>(i * m.cols + m.col[static_cast<std::size_t>(p)])] += m.val[static_cast<std::size_t>(p)];
-  return d;
+  std::vector<double> dense(static_cast<std::size_t>(cells), 0.0);
+  const CooEntries coo = to_coo(m);
+  for (const CooEntry& e : coo.entries) dense[static_cast<std::size_t>(e.row * m.cols + e.col)] += e.value;
+  return dense;
 }
 
 double max_relative_error(const CsrMatrix& a, const CsrMatrix& b) {
   if (!same_pattern(a, b)) throw std::invalid_argument("max_relative_error: patterns differ");
-  double worst = 0.0;
-  for (std::size_t p = 0; p < a.val.size(); ++p) {
-    const double x = a.val[p], y = b.val[p];
-    worst = std::max(worst, std::abs(x - y) / std::max({std::abs(x), std::abs(y), 1.0}));
-  }
-  return worst;
+  // |x - y| / max(|x|, |y|, 1) (csr.cpp:169-181)
+  return std::inner_product(a.val.begin(), a.val.end(), b.val.begin(), 0.0,
+                            [](double acc, double e) { return std::max(acc, e); },
+                            [](double x, double y) {
+                              return std::fabs(x - y) / std::max(1.0, std::max(std::fabs(x), std::fabs(y)));
+                            });
 }
+
+// -------------------------------------------------------------- reference.hpp
+// The reference's statistics and oracle entry points (reference.cpp:9-73).
+// compute_nprod runs kernel K1 on the device; reference_spgemm is the device
+// product with the default (deterministic) options -- C bitwise equal to the
+// reference's row-by-row oracle, whose summation order every numeric kernel keeps.
+offset_t compute_nprod(const CsrMatrix& a, const CsrMatrix& b, std::span<offset_t> out) {
+  if (a.cols != b.rows) throw std::invalid_argument("compute_nprod: a.cols != b.rows");
+  if (out.size() != static_cast<std::size_t>(a.rows))
+    throw std::invalid_argument("compute_nprod: out length != a.rows");
+  const spgemm_csr_view va = view(a), vb = view(b);
+  int64_t total = 0;
+  ok(spgemm_compute_nprod(ctx_for(0), &va, &vb, out.data(), &total));
+  return total;
+}
+
+double compression_ratio(offset_t total_nprod, offset_t total_nnz) {
+  if (total_nnz <= 0) throw std::domain_error("compression_ratio: zero nnz");
+  return static_cast<double>(total_nprod) / static_cast<double>(total_nnz);
+}
+
+MatrixStats input_stats(const CsrMatrix& a) {
+  MatrixStats s;
+  s.rows = a.rows;
+  s.nnz = a.nnz();
+  s.nnz_per_row_mean = a.rows > 0 ? static_cast<double>(s.nnz) / static_cast<double>(a.rows) : 0.0;
+  for (std::size_t i = 1; i < a.rpt.size(); ++i) s.max_nnz_per_row = std::max(s.max_nnz_per_row, a.rpt[i] - a.rpt[i - 1]);
+  return s;
+}
+
+CsrMatrix reference_spgemm(const CsrMatrix& a, const CsrMatrix& b) { return multiply(a, b).c; }
 
 // --------------------------------------------------------------- binning
 BinConfig preset(Phase phase, const std::string& name) {
@@ -438,6 +486,77 @@ SpgemmOutput SpgemmPipeline::collect() {
 }
 
 SpgemmOutput SpgemmPipeline::finish() { return collect(); }
+
+// ------------------------------------------------------ device-resident chain
+DeviceMatrix& DeviceMatrix::operator=(DeviceMatrix&& o) noexcept {
+  if (this != &o) {
+    if (handle_) spgemm_matrix_free(handle_);
+    handle_ = o.handle_;
+    device_ = o.device_;
+    o.handle_ = nullptr;
+  }
+  return *this;
+}
+
+DeviceMatrix::~DeviceMatrix() {
+  if (handle_) spgemm_matrix_free(handle_);
+}
+
+namespace {
+struct Shape {
+  std::int64_t rows = 0, cols = 0, nnz = 0;
+};
+Shape shape_of(const spgemm_matrix* h) {
+  Shape s;
+  if (h) spgemm_matrix_shape(h, &s.rows, &s.cols, &s.nnz);
+  return s;
+}
+}  // namespace
+
+std::int64_t DeviceMatrix::rows() const { return shape_of(handle_).rows; }
+std::int64_t DeviceMatrix::cols() const { return shape_of(handle_).cols; }
+offset_t DeviceMatrix::nnz() const { return shape_of(handle_).nnz; }
+
+CsrMatrix DeviceMatrix::download() const {
+  if (!handle_) throw std::logic_error("DeviceMatrix: empty");
+  const Shape sh = shape_of(handle_);
+  CsrMatrix m;
+  m.rows = sh.rows;
+  m.cols = sh.cols;
+  m.rpt.resize(static_cast<std::size_t>(sh.rows) + 1);
+  m.col.resize(static_cast<std::size_t>(sh.nnz));
+  m.val.resize(static_cast<std::size_t>(sh.nnz));
+  ok(spgemm_matrix_download(ctx_for(device_), handle_, m.rpt.data(), m.col.data(), m.val.data()));
+  return m;
+}
+
+DeviceMatrix multiply_device(const Operand& a, const Operand& b, const SpgemmOptions& options,
+                             SpgemmOutput* stats) {
+  auto operand_view = [&](const Operand& x) {
+    if (x.host()) return view(*x.host());
+    const DeviceMatrix* d = x.device_matrix();
+    if (!d || !d->handle()) throw std::invalid_argument("multiply_device: empty device operand");
+    if (d->device() != options.device)
+      throw std::invalid_argument("multiply_device: operand lives on another device than options.device");
+    spgemm_csr_view v;
+    ok(spgemm_matrix_as_operand(d->handle(), &v));
+    return v;
+  };
+  const spgemm_csr_view va = operand_view(a), vb = operand_view(b);
+  const spgemm_options o = to_c_options(options);
+  spgemm_matrix* c = nullptr;
+  spgemm_report r;
+  ok(spgemm_multiply(ctx_for(options.device), &va, &vb, &o, &c, &r));
+  if (stats) {
+    stats->stats = MatrixStats{r.rows, r.nnz, r.nnz_per_row_mean, r.max_nnz_per_row, r.total_nprod, r.nnz_of_product,
+                               r.cr};
+    stats->timings = StepTimings{r.timings.setup,       r.timings.sym_binning, r.timings.symbolic, r.timings.rpt_alloc,
+                                 r.timings.num_binning, r.timings.numeric,     r.timings.cleanup,  r.timings.total};
+    stats->spilled_rows = r.spilled_rows;
+    stats->workers = r.workers;
+  }
+  return DeviceMatrix(c, options.device);
+}
 
 SpgemmOutput SpgemmPipeline::run() {
   setup();

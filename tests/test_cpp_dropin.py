@@ -32,3 +32,34 @@ def test_reference_unit_tests_on_b200(name):
     res, failed = _run(name)
     assert res.returncode == 0 and not failed, res.stdout[-4000:]
     assert "0 failed" in res.stdout
+
+
+def _run_env(name, env_extra):
+    path = os.path.join(BUILD, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not built (make -C tests/cpp)")
+    env = dict(os.environ, **env_extra)
+    res = subprocess.run([path], capture_output=True, text=True, timeout=900, env=env)
+    failed = [l for l in res.stdout.splitlines() if l.startswith("[FAIL]") or "FAILED" in l]
+    return res, failed
+
+
+def test_product_only_caller_host():
+    """A C++ caller linked against libspgemm_b200.so alone (-Wl,--no-undefined):
+    the reference-header functions it uses are all defined by the product."""
+    res, failed = _run_env("test_product_only", {"SPGEMM_CPP_GPU": "0"})
+    assert res.returncode == 0 and not failed, res.stdout[-3000:]
+
+
+@pytest.mark.gpu
+def test_product_only_caller_gpu():
+    """compute_nprod / reference_spgemm / the device-resident R*(A*P) chain from C++."""
+    res, failed = _run_env("test_product_only", {"SPGEMM_CPP_GPU": "1"})
+    assert res.returncode == 0 and not failed and "0 skipped" in res.stdout, res.stdout[-3000:]
+
+
+@pytest.mark.gpu
+def test_acceptance_criteria_2_3_6_7():
+    """acceptance_main.cpp:141-228, 414-505 against the device path (reference seeds)."""
+    res, failed = _run_env("acceptance_gpu", {})
+    assert res.returncode == 0 and not failed and "0 failed" in res.stdout, res.stdout[-4000:]
