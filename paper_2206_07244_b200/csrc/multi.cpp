@@ -77,6 +77,11 @@ void run_parallel(int32_t n, F work) {
   for (auto& t : threads) t.join();
 }
 
+spgemm_status invalid(const char* msg) {
+  spgemm_internal_set_error(msg);
+  return SPGEMM_INVALID_ARGUMENT;
+}
+
 }  // namespace
 
 extern "C" {
@@ -84,7 +89,8 @@ extern "C" {
 spgemm_status spgemm_multiply_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_csr_view* a,
                                     const spgemm_csr_view* b, const spgemm_options* opts,
                                     spgemm_matrix** slices, int64_t* row_bounds, spgemm_report* report) {
-  if (n < 1 || !ctxs || !a || !b || !slices || !row_bounds) return SPGEMM_INVALID_ARGUMENT;
+  if (n < 1 || !ctxs || !a || !b || !slices || !row_bounds)
+    return invalid("spgemm_multiply_multi: null argument or no devices");
   for (int32_t i = 0; i < n; ++i) slices[i] = nullptr;
   if (n == 1) {
     row_bounds[0] = 0;
@@ -94,9 +100,9 @@ spgemm_status spgemm_multiply_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_c
   if (n > 1 && (a->on_device || b->on_device)) {
     // blocks are staged from host memory to every device; device-resident
     // operands would need peer copies (use the per-GPU process path instead)
-    return SPGEMM_INVALID_ARGUMENT;
+    return invalid("spgemm_multiply_multi: operands must be host-resident when n > 1");
   }
-  if (a->cols != b->rows) return SPGEMM_INVALID_ARGUMENT;
+  if (a->cols != b->rows) return invalid("spgemm: a.cols != b.rows");
   // 1. nprod per row (K1) and the balanced split
   spgemm_status st = split_rows(ctxs[0], n, a, b, row_bounds);
   if (st != SPGEMM_OK) return st;
@@ -144,7 +150,7 @@ spgemm_status spgemm_multiply_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_c
 
 spgemm_status spgemm_matrices_download_stitched(spgemm_ctx** ctxs, spgemm_matrix* const* slices, int32_t n,
                                                 int64_t* rpt, int32_t* col, double* val) {
-  if (n < 1 || !ctxs || !slices || !rpt) return SPGEMM_INVALID_ARGUMENT;
+  if (n < 1 || !ctxs || !slices || !rpt) return invalid("spgemm_matrices_download_stitched: null argument");
   int64_t row = 0, off = 0;
   for (int32_t i = 0; i < n; ++i) {
     int64_t rows = 0, cols = 0, nnz = 0;
@@ -156,7 +162,10 @@ spgemm_status spgemm_matrices_download_stitched(spgemm_ctx** ctxs, spgemm_matrix
                                               val ? val + off : nullptr);
     if (st != SPGEMM_OK) return st;
     for (int64_t r = 0; r <= rows; ++r) rpt[row + r] += off;
-    if (row > 0 && rpt[row] != keep) return SPGEMM_LOGIC_ERROR;
+    if (row > 0 && rpt[row] != keep) {
+      spgemm_internal_set_error("spgemm_matrices_download_stitched: slice offsets disagree");
+      return SPGEMM_LOGIC_ERROR;
+    }
     row += rows;
     off += nnz;
   }
@@ -166,7 +175,7 @@ spgemm_status spgemm_matrices_download_stitched(spgemm_ctx** ctxs, spgemm_matrix
 spgemm_status spgemm_forecast_nnz_multi(spgemm_ctx** ctxs, int32_t n, const spgemm_csr_view* a,
                                         const spgemm_csr_view* b, const spgemm_options* opts, int64_t* row_nnz,
                                         int64_t* row_bounds, int64_t* total_nnz, int64_t* total_nprod) {
-  if (n < 1 || !ctxs || !a || !b) return SPGEMM_INVALID_ARGUMENT;
+  if (n < 1 || !ctxs || !a || !b) return invalid("spgemm_forecast_nnz_multi: null argument or no devices");
   if (n == 1) {
     if (row_bounds) {
       row_bounds[0] = 0;
@@ -174,8 +183,9 @@ spgemm_status spgemm_forecast_nnz_multi(spgemm_ctx** ctxs, int32_t n, const spge
     }
     return spgemm_forecast_nnz(ctxs[0], a, b, opts, row_nnz, total_nnz, total_nprod);
   }
-  if (a->on_device || b->on_device) return SPGEMM_INVALID_ARGUMENT;
-  if (a->cols != b->rows) return SPGEMM_INVALID_ARGUMENT;
+  if (a->on_device || b->on_device)
+    return invalid("spgemm_forecast_nnz_multi: operands must be host-resident when n > 1");
+  if (a->cols != b->rows) return invalid("spgemm: a.cols != b.rows");
   std::vector<int64_t> bounds(static_cast<size_t>(n) + 1);
   spgemm_status st = split_rows(ctxs[0], n, a, b, bounds.data());
   if (st != SPGEMM_OK) return st;
