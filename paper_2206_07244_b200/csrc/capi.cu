@@ -631,13 +631,12 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     // and skewed rows (graphs) rarely fit.
     if (spec.flag != nullptr && G == 32 && u <= 1024 && regular_a && (u > 512 || (u > 256 && avg_b_len >= 16.0))) {
       // speculative numeric first; the symbolic kernel then skips the rows it finished
-      auto sk = &k_num_group<32, 256, 4, 8, int32_t, true>;
-      const int SG = 8;
-      const size_t ssm = static_cast<size_t>(SG) * ((256 + 2) * 8 + kSpecCap * 8 + 256 * 4 + G * 16 + 16);
+      auto sk = &k_num_reuse<true>;
+      const size_t ssm = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
       prepare_kernel(ctx, sk, ssm);
-      const int sgrid = persistent_grid(ctx, sk, G * SG, ssm, ceil_div(rl.count, SG));
-      SPG_LAUNCH(ctx, "k_num_group<" + std::to_string(G) + ",256,spec>", s,
-                 sk<<<sgrid, G * SG, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym, spec));
+      const int sgrid = persistent_grid(ctx, sk, 32 * kReuseWarps, ssm, ceil_div(rl.count, kReuseWarps * kReuseRows));
+      SPG_LAUNCH(ctx, "k_num_reuse<spec>", s,
+                 sk<<<sgrid, 32 * kReuseWarps, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym, spec));
     }
     const size_t smem = static_cast<size_t>(NGRP) * (static_cast<size_t>(std::max(T, WB)) * 4 + G * 16);
     prepare_kernel(ctx, kern, smem);
@@ -864,8 +863,18 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     if (g8) group(NUMG(8, 64, 4, 32), 8, 64, 4, 32);
     else group(NUMG(32, 64, 1, 8), 32, 64, 1, 8);
   } else if (u <= 128) {
-    if (g8) group(NUMG(8, 256, 16, 16), 8, 256, 16, 16);
-    else group(NUMG(32, 256, 4, 8), 32, 256, 4, 8);
+    if (g8) {
+      group(NUMG(8, 256, 16, 16), 8, 256, 16, 16);
+    } else if (idx32 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && std::getenv("SPGEMM_NO_LEAN") == nullptr) {
+      auto kern = &k_num_reuse<false>;
+      const size_t smem = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
+      prepare_kernel(ctx, kern, smem);
+      const int grid = persistent_grid(ctx, kern, 32 * kReuseWarps, smem, ceil_div(rl.count, kReuseWarps * kReuseRows));
+      SPG_LAUNCH(ctx, "k_num_reuse", s,
+                 kern<<<grid, 32 * kReuseWarps, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec));
+    } else {
+      group(NUMG(32, 256, 4, 8), 32, 256, 4, 8);
+    }
   } else if (u <= 256) {
     group(NUMG(32, 512, 8, 8), 32, 512, 8, 8);
   } else if (u <= 512) {

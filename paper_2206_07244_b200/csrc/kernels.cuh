@@ -64,6 +64,7 @@ struct DevInfo {
   long long a_nnz, b_nnz;        // A.rpt[M], B.rpt[B.rows] (device operands: read by K1)
   int tile_counter;
   int pad_;
+  long long b_max_row;           // longest B row any A entry refers to (K1)
 };
 
 constexpr int kErrNumericCount = 1;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kBinThreads)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
-  long long mx = 0, amax = 0;
+  long long mx = 0, amax = 0, bmax = 0;
   unsigned long long tot = 0;
 #pragma unroll 1
   for (int it = 0; it < kRowsPerThread; ++it) {
@@ -400,7 +401,9 @@ __global__ void __launch_bounds__(kBinThreads)
     if (!longrow) {
       for (int64_t p = a0; p < a1; ++p) {
         const int32_t k = A.col[p];
-        n += brpt[k + 1] - brpt[k];
+        const long long l = brpt[k + 1] - brpt[k];
+        n += l;
+        bmax = max(bmax, l);
       }
     }
     unsigned lm = __ballot_sync(kFull, longrow);
@@ -411,7 +414,9 @@ __global__ void __launch_bounds__(kBinThreads)
       long long part = 0;
       for (int64_t p = s0 + lane; p < s1; p += 32) {
         const int32_t k = A.col[p];
-        part += brpt[k + 1] - brpt[k];
+        const long long l = brpt[k + 1] - brpt[k];
+        part += l;
+        bmax = max(bmax, l);
       }
       part = warp_sum(part);
       if (lane == src) n = part;
@@ -425,8 +430,12 @@ __global__ void __launch_bounds__(kBinThreads)
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) amax = max(amax, __shfl_xor_sync(kFull, amax, o));
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = max(amax, __shfl_xor_sync(kFull, amax, o));
+    bmax = max(bmax, __shfl_xor_sync(kFull, bmax, o));
+  }
   if (lane == 0 && amax > 0) atomicMax(&info->a_max_row, amax);
+  if (lane == 0 && bmax > 0) atomicMax(&info->b_max_row, bmax);
   __syncthreads();
   pass1_finish(s_hist, mx, tot, blk_counts, info, s_red);
   if (blockIdx.x == 0 && threadIdx.x == 0) rpt[M] = 0;
@@ -1648,6 +1657,705 @@ __global__ void __launch_bounds__(G* NGRP, (G == 32 && T == 256) ? 5 : 1)
       }
     }
     __syncwarp(gm);
+  }
+}
+
+// Lean ordered numeric for warp-sized rows (3-D stencils, FEM, the RAP chain):
+// one warp per row. A row whose A row has <= 32 entries and whose B rows all
+// have <= 32 entries (the common case for these bins) is walked one A entry per
+// step: lane q takes B(k_j, q), step j+1's loads issued before step j's
+// updates. The column table is sparse (<= 512 slots, load <= 1/4, so a probe
+// rarely goes past the home slot) and maps a column to a DENSE index: the
+// column's values live in vals[0..n) and its column in cols[0..n), in claim
+// order. A step's claims are ranked with one ballot (the claim count is warp-
+// uniform, so a speculative row gives up as soon as it exceeds NMAX, before any
+// out-of-range write). The claiming lane writes the column's first product as
+// 0.0 + x -- the reference's +0.0 start (hash_tables.hpp:130) -- and every
+// later product is a read-modify-write of vals[idx]. Within a step the B row's
+// columns are distinct; __syncwarp orders the steps, so each column folds in
+// the reference's A-row order. No condense pass: the n dense columns are sorted
+// directly (packed with their index) and written with their values.
+// Numeric launches are made only when A's and B's longest rows are <= 32
+// (K1 reports both); a speculative row with longer rows is abandoned.
+constexpr int kLeanGroups = 8;
+constexpr int kLeanT = 512;     // sparse column table slots
+constexpr int kLeanN = 128;     // dense entries (the numeric bin's nnz bound / the speculative cap)
+constexpr size_t kLeanGroupBytes = kLeanT * 4 + kLeanT + kLeanN * 8 + kLeanN * 4 + 32 * 16;
+template <bool SPEC>
+__global__ void __launch_bounds__(32 * kLeanGroups, 5)
+    k_num_lean(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
+               double* __restrict__ cval, uint32_t scale, DevInfo* info, Spec sp) {
+  constexpr int G = 32, NMAX = kLeanN, E = 4;
+  const RowList rl = rl_in.resolved();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* gbase = smem_raw + static_cast<size_t>(grp) * kLeanGroupBytes;
+  int32_t* keys = reinterpret_cast<int32_t*>(gbase);                       // [kLeanT]; after the walk: sort keys
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(gbase);  // (aliases keys: 128 x 8 B)
+  uint32_t* packed32 = reinterpret_cast<uint32_t*>(gbase);
+  uint8_t* sidx = gbase + kLeanT * 4;                                       // [kLeanT] dense index per slot
+  double* vals = reinterpret_cast<double*>(gbase + kLeanT * 5);            // [NMAX]
+  int32_t* cols = reinterpret_cast<int32_t*>(gbase + kLeanT * 5 + NMAX * 8);  // [NMAX]
+  EntryMeta* meta = reinterpret_cast<EntryMeta*>(gbase + kLeanT * 5 + NMAX * 12);
+  const unsigned lt = (1u << lane) - 1u;
+  const Sweep sw(kLeanGroups, grp);
+  for (int64_t idx = sw.first; idx < rl.count; idx += sw.next(idx)) {
+    const int64_t row = rl.row(idx);
+    int64_t base = 0;
+    int n = 0;
+    long long bound;  // >= the row's distinct columns
+    if constexpr (SPEC) {
+      const long long np = rpt[row];
+      if (np == 0) continue;  // no products: the symbolic kernel writes the 0
+      bound = min(np, static_cast<long long>(NMAX));
+    } else {
+      if (sp.done(row)) continue;  // computed in the symbolic phase, copied by k_spec_copy
+      base = rpt[row];
+      n = static_cast<int>(rpt[row + 1] - base);
+      if (n == 0) continue;
+      bound = n;
+    }
+    const int64_t a0 = A.rpt[row], a1 = A.rpt[row + 1];
+    const int na = static_cast<int>(min(a1 - a0, static_cast<int64_t>(1 << 30)));
+    int len = 0;
+    int32_t kmin = 0x7fffffff, kmax = -1;
+    if (lane < na) {
+      const int32_t k = A.col[a0 + lane];
+      const double av = A.val[a0 + lane];
+      const int64_t r0 = B.rpt[k];
+      len = static_cast<int>(B.rpt[k + 1] - r0);
+      meta[lane] = EntryMeta{static_cast<int32_t>(r0), len, av};
+      if (len > 0) {
+        kmin = B.col[r0];
+        kmax = B.col[r0 + len - 1];
+      }
+    }
+    const int maxlen = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(len)));
+    kmin = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<unsigned>(kmin)));
+    kmax = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<unsigned>(kmax + 1))) - 1;
+    int nk = 0;  // distinct columns claimed (warp-uniform)
+    if (na <= G && maxlen <= G) {
+      const int lg = min(log2_const<kLeanT>(), max(2, ceil_log2_ll(4 * bound)));
+      const int tsz = 1 << lg;
+      const Hash hs = make_hash(scale, lg);
+      fill_empty<G>(keys, tsz, lane);
+      __syncwarp();
+      EntryMeta m = meta[0];
+      int32_t cn = lane < m.len ? B.col[m.b0 + lane] : -1;
+      double vn = lane < m.len ? B.val[m.b0 + lane] : 0.0;
+      for (int j = 0; j < na; ++j) {
+        const double a = m.av;
+        const int32_t c = cn;
+        const double bv = vn;
+        if (j + 1 < na) {
+          m = meta[j + 1];
+          cn = lane < m.len ? B.col[m.b0 + lane] : -1;
+          vn = lane < m.len ? B.val[m.b0 + lane] : 0.0;
+        }
+        const double x = __dmul_rn(a, bv);
+        uint32_t h = c >= 0 ? hs.home(c) : 0u;
+        int32_t cur = c >= 0 ? keys[h] : c;
+        bool fresh = false;
+        if (__any_sync(kFull, cur != c)) {
+          while (cur != c) {
+            if (cur == -1) {
+              cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, c);
+              if (cur == -1) {
+                fresh = true;
+                break;
+              }
+              continue;
+            }
+            h = (h + 1) & hs.mask;
+            cur = *reinterpret_cast<volatile int32_t*>(keys + h);
+          }
+        }
+        const unsigned cb = __ballot_sync(kFull, fresh);
+        if constexpr (SPEC) {
+          if (nk + __popc(cb) > NMAX) {  // more columns than the scratch holds: abandon the row
+            nk = NMAX + 1;
+            break;
+          }
+        }
+        if (fresh) {
+          const int ix = nk + __popc(cb & lt);
+          sidx[h] = static_cast<uint8_t>(ix);
+          cols[ix] = c;
+          vals[ix] = __dadd_rn(0.0, x);
+        } else if (c >= 0) {
+          const int ix = sidx[h];
+          vals[ix] = __dadd_rn(vals[ix], x);
+        }
+        nk += __popc(cb);
+        __syncwarp();
+      }
+    } else {
+      // longer A or B rows: never here for numeric launches (the host checks
+      // A's and B's longest rows); a speculative row is left to the symbolic
+      // kernel and the generic numeric kernels
+      nk = NMAX + 1;
+    }
+    __syncwarp();
+    if constexpr (SPEC) {
+      if (nk > NMAX) continue;  // abandoned (uniform): the symbolic kernel counts this row
+      n = nk;
+    } else {
+      if (nk != n && lane == 0) atomicOr(&info->error, kErrNumericCount);
+    }
+    int32_t* ocol = SPEC ? sp.col + row * sp.cap : ccol + base;
+    double* oval = SPEC ? sp.val + row * sp.cap : cval + base;
+    // sort the n columns (with their dense index) and write C(i,:)
+    const bool narrow = static_cast<unsigned>(kmax - kmin) < (1u << 25);
+    for (int e = lane; e < n; e += G) {
+      const int32_t c = cols[e];
+      if (narrow) packed32[e] = (static_cast<uint32_t>(c - kmin) << 7) | static_cast<uint32_t>(e);
+      else packed[e] = (static_cast<unsigned long long>(static_cast<uint32_t>(c)) << 32) | static_cast<uint32_t>(e);
+    }
+    __syncwarp();
+    if (narrow) {
+      group_sort_inplace<G, E, uint32_t>(packed32, n, lane, kFull);
+      __syncwarp();
+      for (int e = lane; e < n; e += G) {
+        const uint32_t v = packed32[e];
+        ocol[e] = kmin + static_cast<int32_t>(v >> 7);
+        oval[e] = vals[v & 127u];
+      }
+    } else {
+      group_sort_inplace<G, E, unsigned long long>(packed, n, lane, kFull);
+      __syncwarp();
+      for (int e = lane; e < n; e += G) {
+        const unsigned long long v = packed[e];
+        ocol[e] = static_cast<int32_t>(v >> 32);
+        oval[e] = vals[static_cast<uint32_t>(v) & 127u];
+      }
+    }
+    if constexpr (SPEC) {
+      if (lane == 0) {
+        rpt[row] = n;
+        sp.flag[row] = 1;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Sort of the n valid keys of buf where the network size is chosen from
+// `nsel` (the same for every group of the warp, so groups sorting different
+// rows stay converged); entries n..network are padded with the maximum key.
+template <int G, int E, typename K>
+__device__ __forceinline__ void group_sort_padded(K* buf, int n, int nsel, int lane, unsigned gm) {
+  if constexpr (E > 1) {
+    if (nsel <= G * E / 2) {
+      group_sort_padded<G, (E > 1 ? E / 2 : 1), K>(buf, n, nsel, lane, gm);
+      return;
+    }
+  }
+  K v[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int e = lane * E + i;
+    v[i] = e < n ? buf[e] : static_cast<K>(~static_cast<K>(0));
+  }
+  group_bitonic<G, E, K>(v, lane, gm);
+#pragma unroll
+  for (int i = 0; i < E; ++i) buf[lane * E + i] = v[i];
+}
+
+// Paired-row ordered numeric (the 3-D stencil / FEM bins): TWO rows per warp,
+// a half-warp (16 lanes) per row, so every per-step instruction -- entry
+// metadata, loads, hashing, the miss vote, the barrier -- serves two rows, and
+// each lane carries two products of the step (B positions q and q+16 of the
+// entry's B row, distinct columns). Preconditions (host-checked for numeric
+// launches, per row for speculative ones): A rows and B rows of <= 32 entries.
+// Per row: a sparse column table of 256 slots (load <= 1/2) mapping a column
+// to a DENSE index -- values in vals[0..n), columns in cols[0..n) in claim
+// order -- claims ranked by ballots within the half-warp. The first product of
+// a column (its claim, in step order) is written as 0.0 + x, the reference's
+// +0.0 start (hash_tables.hpp:130); later products are read-modify-writes;
+// __syncwarp orders the steps (per column: the reference's A-row order). A
+// speculative row abandons (flagged, left to the symbolic kernel) once it
+// claims more than NMAX columns. The n columns are then sorted with their index
+// packed in (the two halves run one network sized for the larger row) and
+// written with their values.
+constexpr int kPairWarps = 8;
+constexpr int kPairT = 256, kPairN = 128;
+constexpr size_t kPairRowBytes = kPairT * 4 + kPairT + kPairN * 8 + kPairN * 4 + 32 * 16;  // 3328
+template <typename T>
+__device__ __forceinline__ T half_min(T v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o, 16));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T half_max(T v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o, 16));
+  return v;
+}
+
+template <bool SPEC>
+__global__ void __launch_bounds__(32 * kPairWarps, 4)
+    k_num_pair(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
+               double* __restrict__ cval, uint32_t scale, DevInfo* info, Spec sp) {
+  constexpr int HG = 16, NMAX = kPairN, E = 8, LOG_T = 8;
+  const RowList rl = rl_in.resolved();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const unsigned hm = 0xffffu << (16 * half);                // this row's lanes
+  const unsigned hlt = ((1u << hl) - 1u) << (16 * half);     // lower lanes of this row
+  unsigned char* rbase = smem_raw + (static_cast<size_t>(warp) * 2 + half) * kPairRowBytes;
+  int32_t* keys = reinterpret_cast<int32_t*>(rbase);  // [kPairT]; after the walk: sort keys
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(rbase);
+  uint32_t* packed32 = reinterpret_cast<uint32_t*>(rbase);
+  uint8_t* sidx = rbase + kPairT * 4;
+  double* vals = reinterpret_cast<double*>(rbase + kPairT * 5);
+  int32_t* cols = reinterpret_cast<int32_t*>(rbase + kPairT * 5 + NMAX * 8);
+  EntryMeta* meta = reinterpret_cast<EntryMeta*>(rbase + kPairT * 5 + NMAX * 12);
+  const int64_t npairs = (rl.count + 1) >> 1;
+  const Sweep sw(kPairWarps, warp);
+  for (int64_t pidx = sw.first; pidx < npairs; pidx += sw.next(pidx)) {
+    const int64_t ridx = 2 * pidx + half;
+    bool live = ridx < rl.count;
+    const int64_t row = live ? rl.row(ridx) : 0;
+    int64_t base = 0;
+    int n = 0;
+    long long bound = 1;
+    if (live) {
+      if constexpr (SPEC) {
+        const long long np = rpt[row];
+        live = np > 0;  // no products: the symbolic kernel writes the 0
+        bound = min(np, static_cast<long long>(NMAX));
+      } else {
+        live = !sp.done(row);  // rows done speculatively are copied by k_spec_copy
+        if (live) {
+          base = rpt[row];
+          n = static_cast<int>(rpt[row + 1] - base);
+          live = n > 0;
+          bound = n;
+        }
+      }
+    }
+    int na = 0, len = 0;
+    int32_t kmin = 0x7fffffff, kmax = -1;
+    if (live) {
+      const int64_t a0 = A.rpt[row];
+      na = static_cast<int>(min(A.rpt[row + 1] - a0, static_cast<int64_t>(33)));
+      for (int q = hl; q < min(na, 32); q += HG) {
+        const int32_t k = A.col[a0 + q];
+        const double av = A.val[a0 + q];
+        const int64_t r0 = B.rpt[k];
+        const int l = static_cast<int>(B.rpt[k + 1] - r0);
+        meta[q] = EntryMeta{static_cast<int32_t>(r0), l, av};
+        len = max(len, l);
+        if (l > 0) {
+          kmin = min(kmin, B.col[r0]);
+          kmax = max(kmax, B.col[r0 + l - 1]);
+        }
+      }
+    }
+    len = half_max(len);
+    kmin = half_min(kmin);
+    kmax = half_max(kmax);
+    if (na > 32 || len > 32) live = false;  // SPEC only: the row is left to the symbolic + generic kernels
+    const int lg = min(LOG_T, max(2, ceil_log2_ll(2 * bound)));
+    const uint32_t hshift = 32u - static_cast<uint32_t>(lg), hmask = (1u << lg) - 1u;
+    const uint32_t mult = scale * 0x9E3779B1u;
+    {
+      int4* t4 = reinterpret_cast<int4*>(keys);
+      for (int s = hl; s < (1 << lg) / 4; s += HG) t4[s] = make_int4(-1, -1, -1, -1);
+    }
+    if (!live) na = 0;
+    const int steps = max(na, __shfl_xor_sync(kFull, na, 16));
+    __syncwarp();
+    int nk = 0;  // this row's claimed columns (uniform within the half)
+    const int32_t* __restrict__ bcol = B.col;
+    const double* __restrict__ bval = B.val;
+    // loads of step j (B positions hl and hl + 16 of the entry's B row)
+    auto load = [&](int j, int32_t& c0, double& v0, int32_t& c1, double& v1, double& a) {
+      c0 = -1;
+      c1 = -1;
+      v0 = 0.0;
+      v1 = 0.0;
+      a = 0.0;
+      if (j < na) {
+        const EntryMeta mm = meta[j];
+        a = mm.av;
+        if (hl < mm.len) {
+          c0 = bcol[mm.b0 + hl];
+          v0 = bval[mm.b0 + hl];
+        }
+        if (hl + HG < mm.len) {
+          c1 = bcol[mm.b0 + hl + HG];
+          v1 = bval[mm.b0 + hl + HG];
+        }
+      }
+    };
+    // one step: both products of the lane (distinct columns of one B row)
+    auto step = [&](double a, int32_t c0, double v0, int32_t c1, double v1) {
+      const double x0 = __dmul_rn(a, v0), x1 = __dmul_rn(a, v1);
+      uint32_t h0 = (static_cast<uint32_t>(c0) * mult) >> hshift;
+      uint32_t h1 = (static_cast<uint32_t>(c1) * mult) >> hshift;
+      int32_t k0 = c0 >= 0 ? keys[h0] : c0;
+      int32_t k1 = c1 >= 0 ? keys[h1] : c1;
+      bool f0 = false, f1 = false;
+      if (__any_sync(kFull, k0 != c0)) {
+        while (k0 != c0) {
+          if (k0 == -1) {
+            k0 = atomicCAS(reinterpret_cast<int*>(keys + h0), -1, c0);
+            f0 = k0 == -1;
+            if (f0) break;
+          } else {
+            h0 = (h0 + 1) & hmask;
+            k0 = *reinterpret_cast<volatile int32_t*>(keys + h0);
+          }
+        }
+      }
+      if (__any_sync(kFull, k1 != c1)) {
+        while (k1 != c1) {
+          if (k1 == -1) {
+            k1 = atomicCAS(reinterpret_cast<int*>(keys + h1), -1, c1);
+            f1 = k1 == -1;
+            if (f1) break;
+          } else {
+            h1 = (h1 + 1) & hmask;
+            k1 = *reinterpret_cast<volatile int32_t*>(keys + h1);
+          }
+        }
+      }
+      const unsigned cb0 = __ballot_sync(kFull, f0) & hm, cb1 = __ballot_sync(kFull, f1) & hm;
+      const int nc0 = __popc(cb0);
+      const int claims = nc0 + __popc(cb1);
+      if (SPEC && nk + claims > NMAX) {  // more columns than the scratch holds: abandon (no write past NMAX)
+        nk = NMAX + 1;
+        na = 0;
+        return;
+      }
+      if (c0 >= 0) {
+        const int ix = f0 ? nk + __popc(cb0 & hlt) : sidx[h0];
+        const double prev = f0 ? 0.0 : vals[ix];
+        vals[ix] = __dadd_rn(prev, x0);
+        if (f0) {
+          sidx[h0] = static_cast<uint8_t>(ix);
+          cols[ix] = c0;
+        }
+      }
+      if (c1 >= 0) {
+        const int ix = f1 ? nk + nc0 + __popc(cb1 & hlt) : sidx[h1];
+        const double prev = f1 ? 0.0 : vals[ix];
+        vals[ix] = __dadd_rn(prev, x1);
+        if (f1) {
+          sidx[h1] = static_cast<uint8_t>(ix);
+          cols[ix] = c1;
+        }
+      }
+      nk += claims;
+    };
+    // two register sets, step j+1's loads in flight during step j
+    int32_t pa0, pa1, pb0, pb1;
+    double ua0, ua1, ub0, ub1, aa, ab;
+    load(0, pa0, ua0, pa1, ua1, aa);
+    for (int j = 0; j < steps; j += 2) {
+      load(j + 1, pb0, ub0, pb1, ub1, ab);
+      step(aa, pa0, ua0, pa1, ua1);
+      __syncwarp();
+      if (j + 1 >= steps) break;
+      load(j + 2, pa0, ua0, pa1, ua1, aa);
+      step(ab, pb0, ub0, pb1, ub1);
+      __syncwarp();
+    }
+    if constexpr (SPEC) {
+      if (nk > NMAX) live = false;  // abandoned
+      n = nk;
+    } else if (live && nk != n && hl == 0) {
+      atomicOr(&info->error, kErrNumericCount);
+    }
+    if (!live) n = 0;
+    // sort the n columns with their dense index; one network for both rows
+    const bool narrow = static_cast<unsigned>(kmax - kmin) < (1u << 25);
+    const bool narrow_all = __all_sync(kFull, narrow || !live);
+    for (int e = hl; e < n; e += HG) {
+      const int32_t c = cols[e];
+      if (narrow_all) packed32[e] = (static_cast<uint32_t>(c - kmin) << 7) | static_cast<uint32_t>(e);
+      else packed[e] = (static_cast<unsigned long long>(static_cast<uint32_t>(c)) << 32) | static_cast<uint32_t>(e);
+    }
+    const int nsel = max(n, __shfl_xor_sync(kFull, n, 16));
+    __syncwarp();
+    if (nsel > 0) {
+      if (narrow_all) group_sort_padded<HG, E, uint32_t>(packed32, n, nsel, hl, kFull);
+      else group_sort_padded<HG, E, unsigned long long>(packed, n, nsel, hl, kFull);
+    }
+    __syncwarp();
+    if (live) {
+      int32_t* ocol = SPEC ? sp.col + row * sp.cap : ccol + base;
+      double* oval = SPEC ? sp.val + row * sp.cap : cval + base;
+      for (int e = hl; e < n; e += HG) {
+        int32_t c;
+        uint32_t ix;
+        if (narrow_all) {
+          const uint32_t v = packed32[e];
+          c = kmin + static_cast<int32_t>(v >> 7);
+          ix = v & 127u;
+        } else {
+          const unsigned long long v = packed[e];
+          c = static_cast<int32_t>(v >> 32);
+          ix = static_cast<uint32_t>(v) & 127u;
+        }
+        ocol[e] = c;
+        oval[e] = vals[ix];
+      }
+      if constexpr (SPEC) {
+        if (hl == 0) {
+          rpt[row] = n;
+          sp.flag[row] = 1;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Structure-reuse numeric for warp-sized rows (3-D stencils, FEM, the RAP
+// chain). One warp per row, a warp takes kReuseRows consecutive rows of its bin.
+// Row i's output STRUCTURE is that of the warp's previous row i' shifted by
+// d = k_1(i) - k_1(i') exactly when both rows have the same number of A
+// entries, entry j's B rows have the same length, and every product column
+// satisfies B(k_j(i), q) - B(k_j(i'), q) = d (with k_j(i) - k_j(i') = d): then
+// the products group into columns the same way, in the same sorted order.
+// The check is exact (every product is compared), so any matrix is handled;
+// translation-invariant structure (interior rows of a grid stencil) passes it.
+// A row that passes skips hashing, claiming and sorting: product (j, q) adds
+// into vals[map[j][q]] -- its output position recorded for row i' -- one A
+// entry per step with __syncwarp between steps (per column the reference's
+// A-row order, starting from +0.0), and C(i,:) is written as
+// (cols(i') + d, vals). A row that fails (or the warp's first row) takes the
+// full path -- the dense-index column table of k_num_lean -- and records the
+// map for the next row. Numeric launches are made only when A's and B's
+// longest rows are <= 32 (K1); a speculative row outside that, or with more
+// than NMAX columns, is abandoned (left to the symbolic kernel).
+constexpr int kReuseWarps = 8;
+constexpr int kReuseRows = 32;  // consecutive rows per warp (power of two)
+constexpr size_t kReuseWarpBytes = 256 * 4 + 256 + 128 * 8 + 128 * 4 + 128 * 4 + 2 * 32 * 16 + 32 * 32;  // 5376
+template <bool SPEC>
+__global__ void __launch_bounds__(32 * kReuseWarps, 5)
+    k_num_reuse(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
+                double* __restrict__ cval, uint32_t scale, DevInfo* info, Spec sp) {
+  constexpr int G = 32, NMAX = 128, T = 256, E = 4;
+  const RowList rl = rl_in.resolved();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = smem_raw + static_cast<size_t>(warp) * kReuseWarpBytes;
+  int32_t* keys = reinterpret_cast<int32_t*>(wb);             // [T]; after the walk: sort keys
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(wb);
+  uint32_t* packed32 = reinterpret_cast<uint32_t*>(wb);
+  uint8_t* sidx = wb + T * 4;                                 // [T] dense index per slot; after: rank
+  double* vals = reinterpret_cast<double*>(wb + T * 5);       // [NMAX]
+  int32_t* cols = reinterpret_cast<int32_t*>(wb + T * 5 + NMAX * 8);      // [NMAX] claim order
+  int32_t* ocols = reinterpret_cast<int32_t*>(wb + T * 5 + NMAX * 12);    // [NMAX] previous row's output
+  EntryMeta* metab = reinterpret_cast<EntryMeta*>(wb + T * 5 + NMAX * 16);  // [2][32]
+  uint8_t* map = wb + T * 5 + NMAX * 16 + 2 * 32 * 16;                   // [32][32] product -> position
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t mult = scale * 0x9E3779B1u;
+  // previous row (warp-uniform except the per-lane entry fields)
+  bool pvalid = false;
+  int pna = 0, pn = 0, mb = 0;
+  int32_t pk = 0;
+  int plen = 0;
+  const int64_t first = (static_cast<int64_t>(blockIdx.x) * kReuseWarps + warp) * kReuseRows;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kReuseWarps * kReuseRows;
+  for (int64_t idx = first; idx < rl.count;
+       idx += (idx & (kReuseRows - 1)) == kReuseRows - 1 ? stride - (kReuseRows - 1) : 1) {
+    const int64_t row = rl.row(idx);
+    int64_t base = 0;
+    int n = 0;
+    long long bound;
+    if constexpr (SPEC) {
+      const long long np = rpt[row];
+      if (np == 0) continue;  // no products: the symbolic kernel writes the 0
+      bound = min(np, static_cast<long long>(NMAX));
+    } else {
+      if (sp.done(row)) continue;  // computed in the symbolic phase, copied by k_spec_copy
+      base = rpt[row];
+      n = static_cast<int>(rpt[row + 1] - base);
+      if (n == 0) continue;
+      bound = n;
+    }
+    EntryMeta* meta = metab + mb * 32;
+    const EntryMeta* pmeta = metab + (mb ^ 1) * 32;
+    const int64_t a0 = A.rpt[row];
+    const int na = static_cast<int>(min(A.rpt[row + 1] - a0, static_cast<int64_t>(33)));
+    int len = 0;
+    int32_t k = 0;
+    double av = 0.0;
+    int32_t b0 = 0;
+    if (lane < na) {
+      k = A.col[a0 + lane];
+      av = A.val[a0 + lane];
+      const int64_t r0 = B.rpt[k];
+      len = static_cast<int>(B.rpt[k + 1] - r0);
+      b0 = static_cast<int32_t>(r0);
+      meta[lane] = EntryMeta{b0, len, av};
+    }
+    const int maxlen = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(len)));
+    if (na > G || maxlen > G) {  // (speculative rows only) left to the symbolic + generic kernels
+      pvalid = false;
+      continue;
+    }
+    __syncwarp();
+    // ---- reuse path
+    const int32_t d = __shfl_sync(kFull, k, 0) - __shfl_sync(kFull, pk, 0);
+    bool reuse = pvalid && na == pna && (SPEC || n == pn) &&
+                 __all_sync(kFull, lane >= na || (len == plen && k - pk == d));
+    if (reuse) {
+      double2* v2 = reinterpret_cast<double2*>(vals);
+      for (int s = lane; s < (pn + 1) / 2; s += G) v2[s] = make_double2(0.0, 0.0);
+      __syncwarp();
+      bool ok = true;
+      for (int j = 0; j < na; ++j) {
+        const EntryMeta m = meta[j];
+        if (lane < m.len) {
+          const int32_t c = B.col[m.b0 + lane];
+          const int32_t cp = B.col[pmeta[j].b0 + lane];
+          const double x = __dmul_rn(m.av, B.val[m.b0 + lane]);
+          ok = ok && c - cp == d;
+          const int pos = map[j * G + lane];
+          vals[pos] = __dadd_rn(vals[pos], x);
+        }
+        if (!__all_sync(kFull, ok)) break;  // structure differs: stop early (the full path recomputes)
+      }
+      if (__all_sync(kFull, ok)) {
+        n = pn;
+        int32_t* ocp = SPEC ? sp.col + row * sp.cap : ccol + base;
+        double* ovp = SPEC ? sp.val + row * sp.cap : cval + base;
+        for (int e = lane; e < n; e += G) {
+          const int32_t c = ocols[e] + d;
+          ocols[e] = c;
+          ocp[e] = c;
+          ovp[e] = vals[e];
+        }
+        if constexpr (SPEC) {
+          if (lane == 0) {
+            rpt[row] = n;
+            sp.flag[row] = 1;
+          }
+        }
+        pk = k;
+        plen = len;
+        mb ^= 1;
+        __syncwarp();
+        continue;
+      }
+      __syncwarp();  // structure differs after all: the full path below
+    }
+    // ---- full path: dense-index column table
+    int32_t kmin = 0x7fffffff, kmax = -1;
+    if (lane < na && len > 0) {
+      kmin = B.col[b0];
+      kmax = B.col[b0 + len - 1];
+    }
+    kmin = static_cast<int32_t>(__reduce_min_sync(kFull, static_cast<unsigned>(kmin)));
+    kmax = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<unsigned>(kmax + 1))) - 1;
+    const int lg = min(log2_const<T>(), max(2, ceil_log2_ll(2 * bound)));
+    const uint32_t hshift = 32u - static_cast<uint32_t>(lg), hmask = (1u << lg) - 1u;
+    fill_empty<G>(keys, 1 << lg, lane);
+    __syncwarp();
+    int nk = 0;
+    for (int j = 0; j < na; ++j) {
+      const EntryMeta m = meta[j];
+      const int32_t c = lane < m.len ? B.col[m.b0 + lane] : -1;
+      const double x = lane < m.len ? __dmul_rn(m.av, B.val[m.b0 + lane]) : 0.0;
+      uint32_t h = (static_cast<uint32_t>(c) * mult) >> hshift;
+      int32_t cur = c >= 0 ? keys[h] : c;
+      bool fresh = false;
+      if (__any_sync(kFull, cur != c)) {
+        while (cur != c) {
+          if (cur == -1) {
+            cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, c);
+            fresh = cur == -1;
+            if (fresh) break;
+          } else {
+            h = (h + 1) & hmask;
+            cur = *reinterpret_cast<volatile int32_t*>(keys + h);
+          }
+        }
+      }
+      const unsigned cb = __ballot_sync(kFull, fresh);
+      if (SPEC && nk + __popc(cb) > NMAX) {  // more columns than the scratch holds: abandon
+        nk = NMAX + 1;
+        break;
+      }
+      if (c >= 0) {
+        const int ix = fresh ? nk + __popc(cb & lt) : sidx[h];
+        const double prev = fresh ? 0.0 : vals[ix];
+        vals[ix] = __dadd_rn(prev, x);
+        map[j * G + lane] = static_cast<uint8_t>(ix);
+        if (fresh) {
+          sidx[h] = static_cast<uint8_t>(ix);
+          cols[ix] = c;
+        }
+      }
+      nk += __popc(cb);
+      __syncwarp();
+    }
+    __syncwarp();
+    if constexpr (SPEC) {
+      if (nk > NMAX) {
+        pvalid = false;
+        continue;  // abandoned (uniform): the symbolic kernel counts this row
+      }
+      n = nk;
+    } else if (nk != n && lane == 0) {
+      atomicOr(&info->error, kErrNumericCount);
+    }
+    // sort the n columns with their dense index; rank[] and the sorted columns
+    const bool narrow = static_cast<unsigned>(kmax - kmin) < (1u << 25);
+    for (int e = lane; e < n; e += G) {
+      const int32_t c = cols[e];
+      if (narrow) packed32[e] = (static_cast<uint32_t>(c - kmin) << 7) | static_cast<uint32_t>(e);
+      else packed[e] = (static_cast<unsigned long long>(static_cast<uint32_t>(c)) << 32) | static_cast<uint32_t>(e);
+    }
+    __syncwarp();
+    if (narrow) group_sort_inplace<G, E, uint32_t>(packed32, n, lane, kFull);
+    else group_sort_inplace<G, E, unsigned long long>(packed, n, lane, kFull);
+    __syncwarp();
+    int32_t* ocp = SPEC ? sp.col + row * sp.cap : ccol + base;
+    double* ovp = SPEC ? sp.val + row * sp.cap : cval + base;
+    uint8_t* rank = sidx;
+    for (int e = lane; e < n; e += G) {
+      int32_t c;
+      uint32_t ix;
+      if (narrow) {
+        const uint32_t v = packed32[e];
+        c = kmin + static_cast<int32_t>(v >> 7);
+        ix = v & 127u;
+      } else {
+        const unsigned long long v = packed[e];
+        c = static_cast<int32_t>(v >> 32);
+        ix = static_cast<uint32_t>(v) & 127u;
+      }
+      ocp[e] = c;
+      ovp[e] = vals[ix];
+      ocols[e] = c;
+      rank[ix] = static_cast<uint8_t>(e);
+    }
+    __syncwarp();
+    // product -> output position for the next row
+    for (int j = 0; j < na; ++j) {
+      if (lane < __shfl_sync(kFull, len, j)) map[j * G + lane] = rank[map[j * G + lane]];
+    }
+    if constexpr (SPEC) {
+      if (lane == 0) {
+        rpt[row] = n;
+        sp.flag[row] = 1;
+      }
+    }
+    pvalid = true;
+    pna = na;
+    pn = n;
+    pk = k;
+    plen = len;
+    mb ^= 1;
+    __syncwarp();
   }
 }
 
