@@ -263,6 +263,21 @@ int persistent_grid(spgemm_ctx* ctx, Kern kern, int threads, size_t smem, int64_
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(work, cap)));
 }
 
+// Rows per warp of the structure-reuse kernel: as many consecutive rows as
+// keep every resident warp busy (long runs let more rows reuse their
+// predecessor; a small bin needs short runs to spread over the SMs).
+// SPGEMM_REUSE_ROWS overrides (experiments).
+template <typename Kern>
+int reuse_rows_per_warp(spgemm_ctx* ctx, Kern kern, size_t smem, int64_t rows) {
+  if (const char* e = std::getenv("SPGEMM_REUSE_ROWS")) return std::max(1, std::min(kReuseRows, std::atoi(e)));
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kReuseWarps, smem), "occupancy");
+  const int64_t warps = static_cast<int64_t>(std::max(per_sm, 1)) * ctx->num_sms * kReuseWarps;
+  int r = kReuseRows;
+  while (r > 1 && rows < warps * r) r >>= 1;
+  return r;
+}
+
 void count_launch(spgemm_ctx* ctx, const char* what) {
   ck(cudaGetLastError(), what);
   ctx->launches.fetch_add(1, std::memory_order_relaxed);
@@ -463,6 +478,7 @@ struct spgemm_pipeline {
   bool heap_ordered() const { return opts.ordered_heap || opts.deterministic; }
   bool heap_bitmap() const { return idx32; }  // bitmap kernels (ordered or atomic); else k_num_global
   int32_t* d_poff = nullptr;                   // ordered bitmap tier: B's column-panel offsets
+  uint8_t* d_shift1 = nullptr;                 // k_num_reuse: B row k == B row k-1 shifted by one (arena)
 };
 
 namespace {
@@ -561,6 +577,10 @@ void spgemm_pipeline::setup() {
   const size_t o_sflag = off, o_scol = align_up(o_sflag + (use_spec ? static_cast<size_t>(M) : 0), 256);
   const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
   if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
+  // the structure-reuse kernels' per-B-row shift flags (warp-sized A and B rows)
+  const bool use_shift = idx32 && M > 0 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && !symbolic_only;
+  const size_t o_shift = off;
+  if (use_shift) off = align_up(o_shift + static_cast<size_t>(std::max<int64_t>(b_rows, 1)), 256);
   arena_bytes = off;
   d_arena = static_cast<unsigned char*>(scratch_acquire(ctx, arena_bytes, s));
   metadata_calls += 1;
@@ -569,6 +589,12 @@ void spgemm_pipeline::setup() {
   d_sums = reinterpret_cast<long long*>(d_arena + o_sums);
   d_bins = reinterpret_cast<int64_t*>(d_arena + o_bins);
   d_spill = reinterpret_cast<int64_t*>(d_arena + o_spill);
+  d_shift1 = nullptr;
+  if (use_shift && b_rows > 0) {
+    d_shift1 = d_arena + o_shift;
+    const int fg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(b_rows, 256)));
+    SPG_LAUNCH(ctx, "k_shift_flags", s, k_shift_flags<<<std::max(fg, 1), 256, 0, s>>>(B, d_shift1));
+  }
   if (use_spec) {
     spec = Spec{reinterpret_cast<int32_t*>(d_arena + o_scol), reinterpret_cast<double*>(d_arena + o_sval),
                 d_arena + o_sflag, kSpecCap};
@@ -634,9 +660,11 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
       auto sk = &k_num_reuse<true>;
       const size_t ssm = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
       prepare_kernel(ctx, sk, ssm);
-      const int sgrid = persistent_grid(ctx, sk, 32 * kReuseWarps, ssm, ceil_div(rl.count, kReuseWarps * kReuseRows));
+      const int rpw = reuse_rows_per_warp(ctx, sk, ssm, rl.count);
+      const int sgrid = persistent_grid(ctx, sk, 32 * kReuseWarps, ssm, ceil_div(rl.count, kReuseWarps * rpw));
       SPG_LAUNCH(ctx, "k_num_reuse<spec>", s,
-                 sk<<<sgrid, 32 * kReuseWarps, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym, spec));
+                 sk<<<sgrid, 32 * kReuseWarps, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym, spec,
+                                                         rpw, d_shift1));
     }
     const size_t smem = static_cast<size_t>(NGRP) * (static_cast<size_t>(std::max(T, WB)) * 4 + G * 16);
     prepare_kernel(ctx, kern, smem);
@@ -869,9 +897,11 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
       auto kern = &k_num_reuse<false>;
       const size_t smem = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
       prepare_kernel(ctx, kern, smem);
-      const int grid = persistent_grid(ctx, kern, 32 * kReuseWarps, smem, ceil_div(rl.count, kReuseWarps * kReuseRows));
+      const int rpw = reuse_rows_per_warp(ctx, kern, smem, rl.count);
+      const int grid = persistent_grid(ctx, kern, 32 * kReuseWarps, smem, ceil_div(rl.count, kReuseWarps * rpw));
       SPG_LAUNCH(ctx, "k_num_reuse", s,
-                 kern<<<grid, 32 * kReuseWarps, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec));
+                 kern<<<grid, 32 * kReuseWarps, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec,
+                                                          rpw, d_shift1));
     } else {
       group(NUMG(32, 256, 4, 8), 32, 256, 4, 8);
     }
@@ -970,6 +1000,9 @@ void spgemm_pipeline::finish(spgemm_report* r) {
   info_to_host(d_info_sym, 0, 2, ctx->main_s);
   ck(cudaStreamSynchronize(ctx->main_s), "cudaStreamSynchronize");
   const DevInfo sym = ctx->h_info[0], num = ctx->h_info[1];
+  if (std::getenv("SPGEMM_DEBUG_REUSE"))
+    std::fprintf(stderr, "reuse: symbolic-phase rows reuse %lld full %lld; numeric rows reuse %lld full %lld\n",
+                 sym.reuse_rows, sym.full_rows, num.reuse_rows, num.full_rows);
   if (num.error & kErrScanMismatch)
     fail(SPGEMM_LOGIC_ERROR, "spgemm: exclusive sum disagrees with binning total");
   if (num.error & kErrNumericCount)

@@ -65,6 +65,7 @@ struct DevInfo {
   int tile_counter;
   int pad_;
   long long b_max_row;           // longest B row any A entry refers to (K1)
+  long long reuse_rows, full_rows;  // k_num_reuse: rows through the reuse / full path
 };
 
 constexpr int kErrNumericCount = 1;
@@ -2139,7 +2140,8 @@ constexpr size_t kReuseWarpBytes = 256 * 4 + 256 + 128 * 8 + 128 * 4 + 128 * 4 +
 template <bool SPEC>
 __global__ void __launch_bounds__(32 * kReuseWarps, 5)
     k_num_reuse(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
-                double* __restrict__ cval, uint32_t scale, DevInfo* info, Spec sp) {
+                double* __restrict__ cval, uint32_t scale, DevInfo* info, Spec sp, int rows_per_warp,
+                const uint8_t* __restrict__ shift1) {
   constexpr int G = 32, NMAX = 128, T = 256, E = 4;
   const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2161,10 +2163,12 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
   int pna = 0, pn = 0, mb = 0;
   int32_t pk = 0;
   int plen = 0;
-  const int64_t first = (static_cast<int64_t>(blockIdx.x) * kReuseWarps + warp) * kReuseRows;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * kReuseWarps * kReuseRows;
-  for (int64_t idx = first; idx < rl.count;
-       idx += (idx & (kReuseRows - 1)) == kReuseRows - 1 ? stride - (kReuseRows - 1) : 1) {
+  // rows_per_warp (a power of two <= kReuseRows) consecutive rows per warp per sweep
+  const int64_t R = rows_per_warp;
+  const int64_t first = (static_cast<int64_t>(blockIdx.x) * kReuseWarps + warp) * R;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kReuseWarps * R;
+  long long nreuse = 0, nfull = 0;  // rows through each path (DevInfo counters)
+  for (int64_t idx = first; idx < rl.count; idx += (idx & (R - 1)) == R - 1 ? stride - (R - 1) : 1) {
     const int64_t row = rl.row(idx);
     int64_t base = 0;
     int n = 0;
@@ -2211,17 +2215,45 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
       for (int s = lane; s < (pn + 1) / 2; s += G) v2[s] = make_double2(0.0, 0.0);
       __syncwarp();
       bool ok = true;
-      for (int j = 0; j < na; ++j) {
-        const EntryMeta m = meta[j];
-        if (lane < m.len) {
-          const int32_t c = B.col[m.b0 + lane];
-          const int32_t cp = B.col[pmeta[j].b0 + lane];
-          const double x = __dmul_rn(m.av, B.val[m.b0 + lane]);
-          ok = ok && c - cp == d;
-          const int pos = map[j * G + lane];
-          vals[pos] = __dadd_rn(vals[pos], x);
+      if (d == 1 && shift1 != nullptr && __all_sync(kFull, lane >= na || shift1[k] != 0)) {
+        // every B row of the row is its predecessor shifted by one column
+        // (precomputed per B row): the structure matches without a per-product
+        // check, and the columns need not be loaded -- only the values, U
+        // steps' loads in flight at once, their updates in step order
+        constexpr int U = 4;
+        for (int j0 = 0; j0 < na; j0 += U) {
+          double bv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const EntryMeta m = meta[min(j0 + u, G - 1)];
+            bv[u] = j0 + u < na && lane < m.len ? B.val[m.b0 + lane] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + u;
+            if (j < na) {
+              const EntryMeta m = meta[j];
+              if (lane < m.len) {
+                const int pos = map[j * G + lane];
+                vals[pos] = __dadd_rn(vals[pos], __dmul_rn(m.av, bv[u]));
+              }
+              __syncwarp();
+            }
+          }
         }
-        if (!__all_sync(kFull, ok)) break;  // structure differs: stop early (the full path recomputes)
+      } else {
+        for (int j = 0; j < na; ++j) {
+          const EntryMeta m = meta[j];
+          if (lane < m.len) {
+            const int32_t c = B.col[m.b0 + lane];
+            const int32_t cp = B.col[pmeta[j].b0 + lane];
+            const double x = __dmul_rn(m.av, B.val[m.b0 + lane]);
+            ok = ok && c - cp == d;
+            const int pos = map[j * G + lane];
+            vals[pos] = __dadd_rn(vals[pos], x);
+          }
+          if (!__all_sync(kFull, ok)) break;  // structure differs: stop early (the full path recomputes)
+        }
       }
       if (__all_sync(kFull, ok)) {
         n = pn;
@@ -2242,6 +2274,7 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
         pk = k;
         plen = len;
         mb ^= 1;
+        ++nreuse;
         __syncwarp();
         continue;
       }
@@ -2355,7 +2388,30 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
     pk = k;
     plen = len;
     mb ^= 1;
+    ++nfull;
     __syncwarp();
+  }
+  if (lane == 0 && (nreuse | nfull)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&info->reuse_rows), static_cast<unsigned long long>(nreuse));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&info->full_rows), static_cast<unsigned long long>(nfull));
+  }
+}
+
+// shift1[k] = 1 when B row k is B row k-1 shifted by one column (same length,
+// every column one larger): the per-B-row precondition that lets k_num_reuse
+// accept a row adjacent to its predecessor (d = 1) without comparing every
+// product's column. Thread per row, 4 entries per load round.
+__global__ void __launch_bounds__(256)
+    k_shift_flags(DevCsr B, uint8_t* __restrict__ shift1) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < B.rows; k += stride) {
+    bool same = false;
+    if (k > 0) {
+      const int64_t r0 = B.rpt[k - 1], r1 = B.rpt[k], r2 = B.rpt[k + 1];
+      same = r2 - r1 == r1 - r0;
+      for (int64_t q = 0; same && q < r2 - r1; ++q) same = B.col[r1 + q] == B.col[r0 + q] + 1;
+    }
+    shift1[k] = same ? 1 : 0;
   }
 }
 
