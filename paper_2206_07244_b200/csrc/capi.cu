@@ -578,7 +578,9 @@ void spgemm_pipeline::setup() {
   const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
   if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
   // the structure-reuse kernels' per-B-row shift flags (warp-sized A and B rows)
-  const bool use_shift = idx32 && M > 0 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && !symbolic_only;
+  // (only the speculative path's products -- regular A, long B rows -- reuse structure)
+  const bool use_shift = idx32 && M > 0 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && !symbolic_only &&
+                         regular_a && avg_b_len > 8.0 && A.rpt == B.rpt;
   const size_t o_shift = off;
   if (use_shift) off = align_up(o_shift + static_cast<size_t>(std::max<int64_t>(b_rows, 1)), 256);
   arena_bytes = off;
@@ -657,14 +659,24 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     // and skewed rows (graphs) rarely fit.
     if (spec.flag != nullptr && G == 32 && u <= 1024 && regular_a && (u > 512 || (u > 256 && avg_b_len >= 16.0))) {
       // speculative numeric first; the symbolic kernel then skips the rows it finished
-      auto sk = &k_num_reuse<true>;
-      const size_t ssm = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
-      prepare_kernel(ctx, sk, ssm);
-      const int rpw = reuse_rows_per_warp(ctx, sk, ssm, rl.count);
-      const int sgrid = persistent_grid(ctx, sk, 32 * kReuseWarps, ssm, ceil_div(rl.count, kReuseWarps * rpw));
-      SPG_LAUNCH(ctx, "k_num_reuse<spec>", s,
-                 sk<<<sgrid, 32 * kReuseWarps, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym, spec,
-                                                         rpw, d_shift1));
+      if (A.rpt == B.rpt) {  // C = A*A: structure reuse (stencil rows repeat)
+        auto sk = &k_num_reuse<true>;
+        const size_t ssm = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
+        prepare_kernel(ctx, sk, ssm);
+        const int rpw = reuse_rows_per_warp(ctx, sk, ssm, rl.count);
+        const int sgrid = persistent_grid(ctx, sk, 32 * kReuseWarps, ssm, ceil_div(rl.count, kReuseWarps * rpw));
+        SPG_LAUNCH(ctx, "k_num_reuse<spec>", s,
+                   sk<<<sgrid, 32 * kReuseWarps, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym,
+                                                           spec, rpw, d_shift1));
+      } else {
+        auto sk = &k_num_lean<true>;
+        const size_t ssm = static_cast<size_t>(kLeanGroups) * kLeanGroupBytes;
+        prepare_kernel(ctx, sk, ssm);
+        const int sgrid = persistent_grid(ctx, sk, 32 * kLeanGroups, ssm, ceil_div(rl.count, kLeanGroups));
+        SPG_LAUNCH(ctx, "k_num_lean<spec>", s,
+                   sk<<<sgrid, 32 * kLeanGroups, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym,
+                                                           spec));
+      }
     }
     const size_t smem = static_cast<size_t>(NGRP) * (static_cast<size_t>(std::max(T, WB)) * 4 + G * 16);
     prepare_kernel(ctx, kern, smem);
@@ -894,14 +906,27 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     if (g8) {
       group(NUMG(8, 256, 16, 16), 8, 256, 16, 16);
     } else if (idx32 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && std::getenv("SPGEMM_NO_LEAN") == nullptr) {
-      auto kern = &k_num_reuse<false>;
-      const size_t smem = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
-      prepare_kernel(ctx, kern, smem);
-      const int rpw = reuse_rows_per_warp(ctx, kern, smem, rl.count);
-      const int grid = persistent_grid(ctx, kern, 32 * kReuseWarps, smem, ceil_div(rl.count, kReuseWarps * rpw));
-      SPG_LAUNCH(ctx, "k_num_reuse", s,
-                 kern<<<grid, 32 * kReuseWarps, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec,
-                                                          rpw, d_shift1));
+      // C = A*A of a regular matrix (stencils: the structure repeats row to
+      // row): structure reuse; other products (the RAP chain's A*P, R*AP):
+      // the dense-index kernel
+      if (spec.flag != nullptr && A.rpt == B.rpt) {
+        auto kern = &k_num_reuse<false>;
+        const size_t smem = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
+        prepare_kernel(ctx, kern, smem);
+        const int rpw = reuse_rows_per_warp(ctx, kern, smem, rl.count);
+        const int grid = persistent_grid(ctx, kern, 32 * kReuseWarps, smem, ceil_div(rl.count, kReuseWarps * rpw));
+        SPG_LAUNCH(ctx, "k_num_reuse", s,
+                   kern<<<grid, 32 * kReuseWarps, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec,
+                                                            rpw, d_shift1));
+      } else {
+        auto kern = &k_num_lean<false>;
+        const size_t smem = static_cast<size_t>(kLeanGroups) * kLeanGroupBytes;
+        prepare_kernel(ctx, kern, smem);
+        const int grid = persistent_grid(ctx, kern, 32 * kLeanGroups, smem, ceil_div(rl.count, kLeanGroups));
+        SPG_LAUNCH(ctx, "k_num_lean", s,
+                   kern<<<grid, 32 * kLeanGroups, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num,
+                                                            spec));
+      }
     } else {
       group(NUMG(32, 256, 4, 8), 32, 256, 4, 8);
     }

@@ -2163,13 +2163,25 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
   int pna = 0, pn = 0, mb = 0;
   int32_t pk = 0;
   int plen = 0;
-  // rows_per_warp (a power of two <= kReuseRows) consecutive rows per warp per sweep
+  // runs of rows_per_warp (<= kReuseRows) consecutive rows per warp per sweep
   const int64_t R = rows_per_warp;
   const int64_t first = (static_cast<int64_t>(blockIdx.x) * kReuseWarps + warp) * R;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kReuseWarps * R;
   long long nreuse = 0, nfull = 0;  // rows through each path (DevInfo counters)
-  for (int64_t idx = first; idx < rl.count; idx += (idx & (R - 1)) == R - 1 ? stride - (R - 1) : 1) {
-    const int64_t row = rl.row(idx);
+  for (int64_t run0 = first; run0 < rl.count; run0 += stride) {
+   // the run's row ids and skip tests, 32 at a time; then its rows in order
+   int64_t lrow = -1;
+   bool need = false;
+   if (lane < R && run0 + lane < rl.count) {
+     lrow = rl.row(run0 + lane);
+     if constexpr (SPEC) need = rpt[lrow] != 0;  // no products: the symbolic kernel writes the 0
+     else need = !sp.done(lrow);                 // rows done speculatively are copied by k_spec_copy
+   }
+   unsigned todo = __ballot_sync(kFull, need);
+   while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1u;
+    const int64_t row = __shfl_sync(kFull, lrow, src);
     int64_t base = 0;
     int n = 0;
     long long bound;
@@ -2220,25 +2232,27 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
         // (precomputed per B row): the structure matches without a per-product
         // check, and the columns need not be loaded -- only the values, U
         // steps' loads in flight at once, their updates in step order
+        // Branch-free: a lane without a product in a step adds 0.0 into the
+        // spare slot vals[NMAX] (it overlays cols[0..1], unused on this path).
         constexpr int U = 4;
+        const double* __restrict__ bval = B.val + lane;
+        const uint8_t* mapl = map + lane;
         for (int j0 = 0; j0 < na; j0 += U) {
-          double bv[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const EntryMeta m = meta[min(j0 + u, G - 1)];
-            bv[u] = j0 + u < na && lane < m.len ? B.val[m.b0 + lane] : 0.0;
-          }
+          double bv[U], av[U];
+          int pos[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int j = j0 + u;
-            if (j < na) {
-              const EntryMeta m = meta[j];
-              if (lane < m.len) {
-                const int pos = map[j * G + lane];
-                vals[pos] = __dadd_rn(vals[pos], __dmul_rn(m.av, bv[u]));
-              }
-              __syncwarp();
-            }
+            const EntryMeta m = meta[(j0 + u) & (G - 1)];
+            const bool on = j < na && lane < m.len;
+            av[u] = m.av;
+            bv[u] = on ? bval[m.b0] : 0.0;
+            pos[u] = on ? mapl[j * G] : NMAX;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            vals[pos[u]] = __dadd_rn(vals[pos[u]], __dmul_rn(av[u], bv[u]));
+            __syncwarp();
           }
         }
       } else {
@@ -2390,6 +2404,7 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
     mb ^= 1;
     ++nfull;
     __syncwarp();
+   }
   }
   if (lane == 0 && (nreuse | nfull)) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&info->reuse_rows), static_cast<unsigned long long>(nreuse));
