@@ -475,6 +475,9 @@ struct spgemm_pipeline {
   // reference's) or options.ordered_heap forces it; bitmap rank +
   // fp64 atomics (within 1e-12, run-to-run bits may differ) only for
   // deterministic=false
+  // A and B of one shape and size (C = A*A, possibly two copies of A): the
+  // products whose rows repeat their neighbours' structure (stencils)
+  bool square_like() const { return A.rows == B.rows && A.cols == B.cols && a_nnz == b_nnz; }
   bool heap_ordered() const { return opts.ordered_heap || opts.deterministic; }
   bool heap_bitmap() const { return idx32; }  // bitmap kernels (ordered or atomic); else k_num_global
   int32_t* d_poff = nullptr;                   // ordered bitmap tier: B's column-panel offsets
@@ -580,7 +583,7 @@ void spgemm_pipeline::setup() {
   // the structure-reuse kernels' per-B-row shift flags (warp-sized A and B rows)
   // (only the speculative path's products -- regular A, long B rows -- reuse structure)
   const bool use_shift = idx32 && M > 0 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && !symbolic_only &&
-                         regular_a && avg_b_len > 8.0 && A.rpt == B.rpt;
+                         regular_a && avg_b_len > 8.0 && square_like();
   const size_t o_shift = off;
   if (use_shift) off = align_up(o_shift + static_cast<size_t>(std::max<int64_t>(b_rows, 1)), 256);
   arena_bytes = off;
@@ -659,7 +662,7 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     // and skewed rows (graphs) rarely fit.
     if (spec.flag != nullptr && G == 32 && u <= 1024 && regular_a && (u > 512 || (u > 256 && avg_b_len >= 16.0))) {
       // speculative numeric first; the symbolic kernel then skips the rows it finished
-      if (A.rpt == B.rpt) {  // C = A*A: structure reuse (stencil rows repeat)
+      if (square_like()) {  // C = A*A-shaped: structure reuse (stencil rows repeat)
         auto sk = &k_num_reuse<true>;
         const size_t ssm = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
         prepare_kernel(ctx, sk, ssm);
@@ -909,7 +912,7 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
       // C = A*A of a regular matrix (stencils: the structure repeats row to
       // row): structure reuse; other products (the RAP chain's A*P, R*AP):
       // the dense-index kernel
-      if (spec.flag != nullptr && A.rpt == B.rpt) {
+      if (spec.flag != nullptr && square_like()) {
         auto kern = &k_num_reuse<false>;
         const size_t smem = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
         prepare_kernel(ctx, kern, smem);
