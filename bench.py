@@ -291,12 +291,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--rmat-scale", type=int, default=24, help="config 5's R-MAT scale (24 = BASELINE)")
+    ap.add_argument("--config", type=int, default=None, choices=[1, 2, 3, 4, 5],
+                    help="default: 2 (the headline) on one GPU; 5 (strong scaling) on N > 1")
+    ap.add_argument("--rmat-scale", type=int, default=None,
+                    help="config 5's R-MAT scale (24 = BASELINE; default 24 on one GPU, 22 for the N > 1 scaling run)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        args.config = 5 if world_env > 1 else 2
+    if args.rmat_scale is None:
+        args.rmat_scale = 22 if world_env > 1 else 24
     if args.impl == "reference":
         return run_reference(args)
     if args.config == 5:
@@ -560,56 +567,61 @@ def main():
 
 
 def run_config5(args):
-    """BASELINE config 5: R-MAT scale 24, C = A*A, nprod ~1e12 and a
-    TB-scale C. Rows are split over the ranks by the nprod prefix (B broadcast once
-    over NCCL); each rank streams its rows through row-block x column-window tiles
-    (paper_2206_07244_b200/tiled.py), every tile a full device pipeline whose C is
-    reduced to checksums and freed. Strong scaling: the product is fixed."""
+    """BASELINE config 5: R-MAT, C = A*A with a TB-scale C, row
+    partitioned across the ranks -- strong scaling (the product is fixed). Rank 0
+    holds A (= B). One step, timed from the broadcast's start to the last tile
+    (SURVEY §8(e) "Timing"): B is broadcast over NCCL with rpt, col and val in
+    flight together; every rank runs K1 as soon as rpt and col have landed
+    (B.val still arriving) and derives the same nprod-balanced row split; its
+    rows are streamed through row-block x 2^20-column-window tiles
+    (paper_2206_07244_b200/tiled.py), each tile a full device pipeline whose C is
+    reduced to checksums and freed. Max time over ranks; GFLOPS counts the whole
+    product's 2*nprod. The ranks' checksums are combined and reported."""
     import torch
     import paper_2206_07244_b200 as sg
     from paper_2206_07244_b200 import synthetic as S
     from paper_2206_07244_b200 import tiled as T
-    from paper_2206_07244_b200.distributed import broadcast_csr, nprod_split
+    from paper_2206_07244_b200.distributed import stream_square_distributed
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group(os.environ.get("SPGEMM_DIST_BACKEND", "nccl"),
-                                device_id=torch.device("cuda", local))
+        backend = os.environ.get("SPGEMM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     ctx = sg.get_context(local)
     t0 = time.perf_counter()
     a_host = S.rmat(args.rmat_scale, 16, seed=args.rmat_scale) if rank == 0 else None
     gen_s = time.perf_counter() - t0
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if dist:
-        dist.barrier()
-        B = broadcast_csr(a_host.to_device(local) if rank == 0 else None, 0, torch.device("cuda", local))
-    else:
-        B = a_host.to_device(local)
-    torch.cuda.synchronize()
-    bcast_s = time.perf_counter() - t0
-    nprod, total = sg.compute_nprod(B, B, device=local)
-    bounds = nprod_split(nprod, world)
-    rows = range(bounds[rank], bounds[rank + 1])
-    t0 = time.perf_counter()
-    wins = T.split_columns(B)
-    torch.cuda.synchronize()
-    split_s = time.perf_counter() - t0
+    a_dev = a_host.to_device(local) if rank == 0 else None
     budget = int(os.environ.get("SPGEMM_TILE_BUDGET", 12_000_000_000))
     workers = int(os.environ.get("SPGEMM_TILE_WORKERS", 3))  # measured best at scale 22 (1: 4.2 s, 3: 3.5 s)
+    bcast = "on" if world > 1 else "none (one GPU)"
+
+    def local_stream(B, rows, nprod):
+        return T.stream_multiply(B, B, rows=rows, nprod=nprod, b_windows=T.split_columns(B), budget=budget,
+                                 device=local, workers=workers)
 
     def step():
-        return T.stream_multiply(B, B, rows=rows, nprod=nprod, b_windows=wins, budget=budget, device=local,
-                                 workers=workers)
+        l0 = ctx.kernel_launches
+        if dist:
+            res = stream_square_distributed(a_dev if rank == 0 else None, device=dev, local_stream=local_stream)
+            rep, total = res.local, res.total_nprod
+        else:
+            nprod, total = sg.compute_nprod(a_dev, a_dev, device=local)
+            rep = local_stream(a_dev, range(0, a_dev.rows), nprod)
+        return rep, total, ctx.kernel_launches - l0
 
     for _ in range(max(3, args.warmup)):
-        rep = step()
-    stream = torch.cuda.ExternalStream(ctx.stream)
+        step()
+    stream = torch.cuda.current_stream()
     clocks = ClockSampler(local)
     if dist:
         dist.barrier()
@@ -621,57 +633,70 @@ def run_config5(args):
     ev0.record(stream)
     launches = 0
     nprod_done = 0
+    local_nprod = 0
     for _ in range(args.steps):
-        rep = step()
-        nprod_done += rep.total_nprod
-        launches += rep.kernel_launches
+        rep, total, nl = step()
+        nprod_done += total
+        local_nprod += rep.total_nprod
+        launches += nl + rep.kernel_launches
     ev1.record(stream)
     torch.cuda.synchronize()
     tw1 = time.time()
     if rank == 0:
         clocks.stop()
     t_ms = ev0.elapsed_time(ev1)
+    nnz_all, vsum, phash = rep.nnz, rep.val_sum, rep.pattern_hash
+    per_rank_ms = [t_ms]
     if dist:
         dist.barrier()
         tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-        nn = torch.tensor([nprod_done, rep.nnz], dtype=torch.int64, device="cuda")
+        gathered = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(world)]
+        dist.all_gather(gathered, tt)
+        per_rank_ms = [float(g.item()) for g in gathered]
+        t_ms = max(per_rank_ms)
+        nn = torch.tensor([rep.nnz, local_nprod, launches], dtype=torch.int64, device="cuda")
         dist.all_reduce(nn)
-        nprod_done, nnz_all = (int(x) for x in nn.tolist())
-    else:
-        nnz_all = rep.nnz
+        nnz_all, local_sum, launches = (int(x) for x in nn.tolist())
+        assert local_sum == nprod_done, "the ranks' row blocks must cover the product exactly"
+        vs = torch.tensor([vsum], dtype=torch.float64, device="cuda")
+        dist.all_reduce(vs)
+        vsum = float(vs.item())
+        hh = torch.tensor([phash & ((1 << 62) - 1)], dtype=torch.int64, device="cuda")
+        dist.all_reduce(hh)
+        phash = int(hh.item())
     if rank == 0:
         value = 2 * nprod_done / (t_ms * 1e-3) / 1e9
         ms = t_ms / args.steps
-        # algorithmic bytes per step: A + B + C, C counted once as streamed through HBM
-        a_nnz = B.nnz()
-        step_bytes = 2 * csr_bytes(B.rows, a_nnz) + csr_bytes(B.rows, nnz_all)
+        step_bytes = 2 * csr_bytes(a_host.rows, a_host.nnz()) + csr_bytes(a_host.rows, nnz_all)
         peak, peak_kind = load_peaks()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[5], "rmat_scale": args.rmat_scale, "nprod_per_step": total,
-                       "nnz_c": nnz_all, "tiles_per_step_rank0": rep.tiles, "window_cols": T.WINDOW,
+            "config": {"workload": CONFIG_NAMES[5].replace("scale 24", f"scale {args.rmat_scale}"),
+                       "rmat_scale": args.rmat_scale,
+                       "nprod_per_step": nprod_done // args.steps, "nnz_c": nnz_all, "window_cols": T.WINDOW,
                        "tile_budget_nprod": budget, "tile_workers": workers,
-                       "parallelism": f"row-block dp{world}",
+                       "parallelism": f"row-block dp{world}", "b_broadcast": bcast,
+                       "timed": "broadcast start (N>1) to the last tile of every rank, max over ranks",
                        "l2": "inputs larger than L2", "generate_s": round(gen_s, 1),
-                       "b_broadcast_s": round(bcast_s, 3), "b_split_s": round(split_s, 3)},
+                       "per_rank_ms_per_step": [round(x / args.steps, 2) for x in per_rank_ms],
+                       "note": ("strong scaling at R-MAT scale %d (scale 24 = BASELINE config 5: "
+                                "bench.py --config 5 --rmat-scale 24)" % args.rmat_scale)
+                       if args.rmat_scale != 24 else "BASELINE config 5"},
             "roofline": None,
             "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9,
                               "frac": step_bytes / (ms * 1e-3) / 1e9 / peak, "peak": peak, "peak_source": peak_kind},
             "cpu_baseline": None,
             "e2e": {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "note": "C is TB-scale: streamed to checksums on the device, never copied to the host"},
-            "checksums": {"nnz": nnz_all, "val_sum_rank0": rep.val_sum, "pattern_hash_rank0": rep.pattern_hash},
+            "checksums": {"nnz": nnz_all, "val_sum": vsum, "pattern_hash_mod_2^62": phash & ((1 << 62) - 1)},
             "gpu_launches": launches,
             "clocks": clocks.summary(tw0, tw1),
         }
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cpu = cpu_baseline(a_host, rows_frac=0.0005, runs=1)
-                line["cpu_baseline"] = cpu
+                line["cpu_baseline"] = cpu_baseline(a_host, rows_frac=0.0005, runs=1)
             except Exception as e:  # pragma: no cover
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                                         "sample": str(e)}

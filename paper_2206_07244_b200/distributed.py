@@ -241,3 +241,89 @@ def forecast_distributed(a: Optional[CsrMatrix], b: Optional[CsrMatrix], *, same
     t = torch.tensor([local], dtype=torch.int64, device=dev)
     dist.all_reduce(t, group=group)
     return DistributedForecast(int(t.item()), int(nprod.sum()), local, bounds, rows)
+
+
+# ---------------------------------------------------------------------------
+# Streamed, row-partitioned C = B*B with the broadcast inside the step (config
+# 5 strong scaling, SURVEY.md §8(e) "Collective" and "Timing" rows).
+@dataclass
+class PendingCsr:
+    """A broadcast CSR matrix whose arrays may still be in flight."""
+    m: CsrMatrix
+    works: dict
+
+    def wait(self, *names: str) -> None:
+        for n in names:
+            w = self.works.pop(n, None)
+            if w is not None:
+                w.wait()  # NCCL: the current CUDA stream waits (no host block); gloo: blocks
+
+
+def broadcast_csr_async(m: Optional[CsrMatrix], src: int = 0, device=None, group=None) -> PendingCsr:
+    """broadcast_csr with the three array broadcasts issued asynchronously, B.rpt
+    first, then B.col, then B.val (one NCCL stream, in that order): K1 needs only
+    rpt and col, so B.val's transfer overlaps it (and the row split)."""
+    import torch
+    dist = _dist()
+    rank = dist.get_rank(group)
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    if rank == src:
+        shape = torch.tensor([m.rows, m.cols, m.nnz()], dtype=torch.int64, device=dev)
+    else:
+        shape = torch.zeros(3, dtype=torch.int64, device=dev)
+    dist.broadcast(shape, src, group=group)
+    rows, cols, nnz = (int(x) for x in shape.tolist())
+    if rank == src:
+        if m.on_device and dev.type == "cuda":
+            rpt, col, val = m.rpt, m.col, m.val
+        else:
+            h = m.to_host()
+            rpt, col, val = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (h.rpt, h.col, h.val))
+    else:
+        rpt = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+        col = torch.empty(nnz, dtype=torch.int32, device=dev)
+        val = torch.empty(nnz, dtype=torch.float64, device=dev)
+    works = {}
+    for name, t in (("rpt", rpt), ("col", col), ("val", val)):
+        works[name] = dist.broadcast(t, src, group=group, async_op=True) if t.numel() else None
+    if dev.type == "cuda":
+        out = CsrMatrix(rows, cols, rpt, col, val)
+    else:
+        out = CsrMatrix(rows, cols, rpt.numpy(), col.numpy(), val.numpy())
+    return PendingCsr(out, works)
+
+
+@dataclass
+class StreamedResult:
+    row_bounds: List[int]
+    total_nprod: int          # of the whole product (every rank's K1 sees all of it)
+    local: object             # this rank's tiles' report (tiled.StreamReport or the injected equivalent)
+
+
+def stream_square_distributed(b: Optional[CsrMatrix], *, src: int = 0, device=None, group=None,
+                              local_nprod: Optional[Callable] = None,
+                              local_stream: Optional[Callable] = None) -> StreamedResult:
+    """One step of the config-5 strong-scaling workload, C = B*B with B on rank
+    `src` only: B is broadcast (rpt, col, val in flight together); each rank runs
+    K1 as soon as rpt and col have landed -- B.val's transfer overlaps it -- and
+    derives the same nprod-balanced row split; then its row block is streamed
+    through row-block x column-window tiles (tiled.stream_multiply). No further
+    collective: the caller reduces the checksums and the max time."""
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if local_nprod is None:
+        from . import api as sg
+        dev_index = None if device is None else (device.index if hasattr(device, "index") else int(str(device).split(":")[-1]))
+
+        def local_nprod(x, y):  # noqa: E306
+            return sg.compute_nprod(x, y, device=dev_index)[0]
+    if local_stream is None:
+        raise ValueError("local_stream(B, rows, nprod) is required")
+    pend = broadcast_csr_async(b if rank == src else None, src, device, group)
+    B = pend.m
+    pend.wait("rpt", "col")
+    nprod = np.asarray(local_nprod(B, B), np.int64)   # K1 while B.val is still arriving
+    bounds = nprod_split(nprod, world)
+    pend.wait("val")
+    rep = local_stream(B, range(bounds[rank], bounds[rank + 1]), nprod)
+    return StreamedResult(bounds, int(nprod.sum()), rep)

@@ -145,3 +145,69 @@ def test_stitch_offsets():
     parts = [slice_rows(a, 0, 17), slice_rows(a, 17, 17), slice_rows(a, 17, 50)]
     s = stitch(parts, a.cols)
     assert isinstance(s, CsrMatrix) and s == a
+
+
+def _worker_streamed(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    from oracle import oracle as O
+    from paper_2206_07244_b200 import synthetic as S
+    from paper_2206_07244_b200.distributed import slice_rows, stream_square_distributed
+    from paper_2206_07244_b200.tiled import checksum_of
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b = S.random_values(S.rmat(9, 16, seed=9), 4) if rank == 0 else None
+
+        def local_stream(B, rows, nprod):  # the per-rank tiles, checked with the oracle on CPU
+            from paper_2206_07244_b200.api import CsrMatrix
+            c = O.spgemm(slice_rows(B, rows.start, rows.stop), B)
+            c = CsrMatrix(c.rows, c.cols, c.rpt, c.col, c.val)
+            cs = checksum_of(c)
+            # global row numbers in the pattern hash, as tiled.stream_multiply reports them
+            rr = np.repeat(np.arange(c.rows, dtype=np.uint64) + np.uint64(rows.start + 1), np.diff(c.rpt))
+            cs.pattern_hash = int(np.sum((c.col.astype(np.uint64) + np.uint64(1)) * rr, dtype=np.uint64))
+            return cs
+
+        res = stream_square_distributed(b, local_nprod=lambda x, y: O.compute_nprod(x, y)[0],
+                                        local_stream=local_stream)
+        t = torch.tensor([res.local.nnz, res.local.pattern_hash & ((1 << 62) - 1)], dtype=torch.int64)
+        parts = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, t)
+        out = dict(rank=rank, bounds=res.row_bounds, total=res.total_nprod, nnz=[int(p[0]) for p in parts],
+                   hashes=[int(p[1]) for p in parts], hash_full=res.local.pattern_hash, vsum=res.local.val_sum)
+        if rank == 0:
+            from paper_2206_07244_b200.api import CsrMatrix
+            exp = O.spgemm(b, b)
+            full = checksum_of(CsrMatrix(exp.rows, exp.cols, exp.rpt, exp.col, exp.val))
+            out["exp_nnz"], out["exp_hash"], out["exp_vsum"] = full.nnz, full.pattern_hash, full.val_sum
+            out["exp_total"] = O.compute_nprod(b, b)[1]
+        q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_streamed_square_with_async_broadcast():
+    """stream_square_distributed (bench.py's multi-GPU step): B broadcast with rpt/col/val
+    in flight together, K1 after rpt+col, the nprod split, each rank's row block --
+    the ranks' checksums add up to the single-shot product's."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_streamed, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted((q.get(timeout=180) for _ in procs), key=lambda d: d["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    r0, r1 = outs
+    assert r0["bounds"] == r1["bounds"]
+    assert r0["total"] == r1["total"] == r0["exp_total"]
+    assert sum(r0["nnz"]) == r0["exp_nnz"]
+    assert (r0["hash_full"] + r1["hash_full"]) % (1 << 64) == r0["exp_hash"]
+    assert abs(r0["vsum"] + r1["vsum"] - r0["exp_vsum"]) <= 1e-9 * max(1.0, abs(r0["exp_vsum"]))
