@@ -110,3 +110,35 @@ def test_rmat20_config3_sampled(sg, oracle):
     a = S.rmat(20, 16, seed=20)
     out = _check_sampled(sg, oracle, a, 20, n_random=200)
     assert out.stats.total_nprod > 2e10 and out.spilled_rows > 0
+
+
+@pytest.mark.slow
+def test_rmat24_config5_sampled(sg, oracle):
+    """BASELINE config 5 (R-MAT scale 24, nprod 1.0e12, C ~6 TB: never materialised)
+    checked at its own size on a deterministic row sample (SURVEY.md §8(d)
+    "Verification for large configs"): every row with nprod > 1e8, the heaviest
+    rows below that, 256 consecutive rows of the middle of the matrix (the bench's
+    cpu_baseline block) and random rows -- C(sample, :) from the device against the
+    REFERENCE's own pipeline (oracle/_ref, spgemm::multiply) on the same rows:
+    structure bitwise, values bitwise (deterministic mode)."""
+    a = S.random_values(S.rmat(24, 16, seed=24), 24)
+    import torch
+    d = a.to_device()
+    nprod, total = sg.compute_nprod(d, d)
+    assert total > 1.0e12
+    rng = np.random.default_rng(24)
+    order = np.argsort(nprod)[::-1]
+    heavy = np.nonzero(nprod > 100_000_000)[0]
+    mid = a.rows // 2
+    sample = np.unique(np.concatenate([heavy, order[:8], np.arange(mid, mid + 256),
+                                       rng.choice(a.rows, 256, replace=False)]))
+    sub = _rows_subset(a, sample)
+    got = sg.multiply(sub.to_device(), d)
+    if oracle.ref_available():
+        exp, info = oracle.ref_multiply(sub, a)
+        assert info["total_nprod"] == int(nprod[sample].sum())
+    else:
+        exp = oracle.spgemm(sub, a)
+    assert_matches_oracle(got.c, exp)
+    del d
+    torch.cuda.empty_cache()
