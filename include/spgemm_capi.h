@@ -150,8 +150,12 @@ typedef struct spgemm_kernel_time {
   double total_ms;
 } spgemm_kernel_time;
 void spgemm_ctx_set_profiling(spgemm_ctx* ctx, int32_t on);
-/* Stream-ordered pool of the device: bytes reserved from the driver / in use. */
+/* The context's private stream-ordered pool: bytes reserved from the driver / in use. */
 spgemm_status spgemm_ctx_pool_stats(spgemm_ctx* ctx, uint64_t* reserved, uint64_t* used);
+/* Gives the context's cached scratch (metadata arenas, staged inputs) back to
+ * its private stream-ordered pool and trims the pool to keep_bytes of reserved
+ * memory (synchronises the context's streams). */
+spgemm_status spgemm_ctx_trim(spgemm_ctx* ctx, uint64_t keep_bytes);
 int32_t spgemm_ctx_profile_summary(spgemm_ctx* ctx, spgemm_kernel_time* out, int32_t max);
 
 /* ------------------------------------------------------- configuration */

@@ -128,6 +128,10 @@ class Context:
         _check(_c.lib.spgemm_ctx_pool_stats(self.handle, C.byref(r), C.byref(u)))
         return r.value, u.value
 
+    def trim(self, keep_bytes: int = 0) -> None:
+        """Return cached scratch and pooled HBM beyond keep_bytes to the driver."""
+        _check(_c.lib.spgemm_ctx_trim(self.handle, int(keep_bytes)))
+
     def profile_summary(self) -> dict:
         """{kernel name: (launches, total ms)} since the last call (synchronises)."""
         buf = (_c.KernelTime * 64)()

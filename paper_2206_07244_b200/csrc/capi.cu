@@ -213,6 +213,7 @@ struct spgemm_ctx {
     bool busy;
   };
   std::vector<Scratch> scratch;
+  cudaMemPool_t pool = nullptr;  // this context's stream-ordered pool
 };
 
 namespace {
@@ -330,12 +331,15 @@ struct LaunchScope {
 // (concurrent bins would fold their co-resident neighbours into its duration).
 cudaStream_t bin_stream(spgemm_ctx* ctx, int bin) { return ctx->prof ? ctx->main_s : ctx->bin_s[bin]; }
 
-void* dev_alloc(size_t bytes, cudaStream_t s) {
+// Stream-ordered allocations come from the context's own memory pool (not the
+// device's default pool, whose settings other libraries in the process rely on).
+void* dev_alloc_ctx(spgemm_ctx* ctx, size_t bytes, cudaStream_t s) {
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
-  ck(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+  ck(cudaMallocFromPoolAsync(&p, bytes, ctx->pool, s), "cudaMallocFromPoolAsync");
   return p;
 }
+#define dev_alloc(BYTES, STREAM) dev_alloc_ctx(ctx, (BYTES), (STREAM))
 
 void dev_free(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
@@ -1141,17 +1145,23 @@ spgemm_status spgemm_ctx_create(int32_t device, spgemm_ctx** out) {
       ck(cudaHostAlloc(&c->h_info, 2 * sizeof(DevInfo), cudaHostAllocMapped | cudaHostAllocPortable),
          "cudaHostAlloc");
       ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_info_dev), c->h_info, 0), "cudaHostGetDevicePointer");
-      // Keep freed blocks in the stream-ordered pool: repeated multiplies
-      // reuse HBM without returning it to the driver.
-      cudaMemPool_t pool;
-      ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+      // A private stream-ordered pool (the device's default pool is left as
+      // other users of the process configured it). Freed blocks stay in the
+      // pool, so repeated multiplies reuse HBM without returning it to the
+      // driver; spgemm_ctx_trim gives it back.
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      ck(cudaMemPoolCreate(&c->pool, &props), "cudaMemPoolCreate");
       uint64_t thresh = std::numeric_limits<uint64_t>::max();
-      ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh), "pool attr");
+      ck(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh), "pool attr");
       // Never make an allocation wait on another stream's free: C freed on the
       // copy lane behind its download must not stall the next product's
       // kernels (the pool takes fresh memory instead).
       int no = 0;
-      ck(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no), "pool attr");
+      ck(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &no), "pool attr");
     } catch (...) {
       spgemm_ctx_destroy(c);
       throw;
@@ -1180,10 +1190,29 @@ void spgemm_ctx_destroy(spgemm_ctx* c) {
     cudaEventDestroy(r.b);
   }
   for (auto& e : c->ev_pool) cudaEventDestroy(e);
-  for (auto& b : c->scratch) cudaFree(b.p);
+  for (auto& b : c->scratch) cudaFreeAsync(b.p, 0);
+  cudaDeviceSynchronize();
+  // (result matrices still alive keep the pool's memory until they are freed)
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   if (c->h_info) cudaFreeHost(c->h_info);
   if (prev >= 0) cudaSetDevice(prev);
   delete c;
+}
+
+spgemm_status spgemm_ctx_trim(spgemm_ctx* c, uint64_t keep_bytes) {
+  return guard([&] {
+    DeviceGuard g(c->device);
+    ck(cudaStreamSynchronize(c->main_s), "cudaStreamSynchronize");
+    ck(cudaStreamSynchronize(c->side_s), "cudaStreamSynchronize");
+    std::vector<spgemm_ctx::Scratch> keep;
+    for (auto& b : c->scratch) {
+      if (b.busy) keep.push_back(b);
+      else ck(cudaFreeAsync(b.p, c->main_s), "cudaFreeAsync");
+    }
+    c->scratch.swap(keep);
+    ck(cudaStreamSynchronize(c->main_s), "cudaStreamSynchronize");
+    ck(cudaMemPoolTrimTo(c->pool, static_cast<size_t>(keep_bytes)), "cudaMemPoolTrimTo");
+  });
 }
 
 int32_t spgemm_ctx_device(const spgemm_ctx* c) { return c->device; }
@@ -1194,10 +1223,8 @@ void spgemm_ctx_set_profiling(spgemm_ctx* c, int32_t on) { c->prof = on != 0; }
 
 spgemm_status spgemm_ctx_pool_stats(spgemm_ctx* c, uint64_t* reserved, uint64_t* used) {
   return guard([&] {
-    cudaMemPool_t pool;
-    ck(cudaDeviceGetMemPool(&pool, c->device), "cudaDeviceGetMemPool");
-    ck(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, reserved), "pool attr");
-    ck(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, used), "pool attr");
+    ck(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, reserved), "pool attr");
+    ck(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemCurrent, used), "pool attr");
   });
 }
 

@@ -52,3 +52,23 @@ def test_multiply_into_zero_rows(sg):
     b = random_csr(5, 7, 0.5, 1)
     rpt, col, val = _bufs(0, 0)
     assert sg.multiply_into(a, b, rpt, col, val)[0] == 0 and rpt[0] == 0
+
+
+def test_private_pool_and_trim(sg):
+    """The library allocates from its context's own stream-ordered pool:
+    Context.trim() returns the cached scratch and pooled HBM, and the context
+    keeps working after it."""
+    import torch
+    from paper_2206_07244_b200 import synthetic as S
+    ctx = sg.get_context(0)
+    a = S.stencil3d_27pt(40)
+    out = sg.multiply(a, a)
+    assert out.c.nnz() > 0
+    reserved, used = ctx.pool_stats()
+    assert reserved > 0
+    ctx.trim(0)
+    r2, u2 = ctx.pool_stats()
+    assert r2 <= reserved and u2 == 0
+    # a further multiply works after the trim (the pool regrows)
+    assert sg.multiply(a, a).c.nnz() == out.c.nnz()
+    torch.cuda.synchronize()

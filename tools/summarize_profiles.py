@@ -25,11 +25,13 @@ def short_name(full):
     if targs:
         args = [a.strip().replace("(int)", "") for a in targs[1:-1].split(",")]
         keep = [a for a in args if a.isdigit()]
+        last = targs[1:-1].split(",")[-1].strip().replace("(bool)", "")
         if name in ("k_sym_group", "k_num_group"):
             keep = keep[:2]
-            last = targs[1:-1].split(",")[-1].strip().replace("(bool)", "")
             if name == "k_num_group" and last in ("1", "true"):
                 keep.append("spec")  # the speculative instance of the symbolic phase
+        elif name in ("k_num_lean", "k_num_reuse", "k_num_pair"):
+            keep = ["spec"] if last in ("1", "true") else []
         elif name in ("k_sym_block", "k_num_block"):
             keep = keep[:1]
         targs = "<" + ",".join(keep) + ">" if keep else ""
@@ -69,25 +71,38 @@ def full(rep, out_json, out_md=None):
             "l2_hit_pct": f("lts__t_sector_hit_rate.pct"),
             "registers": f("launch__registers_per_thread"),
             "smem_bank_conflicts": f("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
-            "shared_atomics": f("l1tex__t_requests_pipe_lsu_mem_shared_op_atom.sum"),
+            "shared_atomic_instructions": f("smsp__inst_executed_op_shared_atom.sum"),
+            "global_red_instructions": f("smsp__inst_executed_op_global_red.sum"),
+            "global_atomic_instructions": f("smsp__inst_executed_op_global_atom.sum"),
+            "shared_load_instructions": f("smsp__sass_inst_executed_op_shared_ld.sum"),
+            "global_load_instructions": f("smsp__sass_inst_executed_op_global_ld.sum"),
+            "l2_sectors": f("lts__t_sectors.sum"),
             "top_stalls": top,
         }
         if rec["dram_bytes_read"] is not None and rec["dram_bytes_write"] is not None:
             rec["dram_bytes_per_launch"] = rec["dram_bytes_read"] + rec["dram_bytes_write"]
             rec["dram_gbs"] = rec["dram_bytes_per_launch"] / (dur_ms * 1e-3) / 1e9
-        kernels.setdefault(name, rec)
+        if name in kernels:  # several launches of one kernel (bins): keep each
+            i = 2
+            while f"{name}#{i}" in kernels:
+                i += 1
+            name = f"{name}#{i}"
+        kernels[name] = rec
     with open(out_json, "w") as fh:
         json.dump({"source": rep, "kernels": kernels}, fh, indent=1)
     if out_md:
         with open(out_md, "w") as fh:
             fh.write(f"# ncu --set full summary ({rep.split('/')[-1]})\n\n")
-            fh.write("| kernel | ms | DRAM GB (r+w) | DRAM GB/s | IPC | occ % | L1 hit % | L2 hit % | smem bank conflicts | top stalls |\n")
-            fh.write("|---|---|---|---|---|---|---|---|---|---|\n")
+            fh.write("| kernel | ms | DRAM GB (r+w) | DRAM GB/s | IPC | occ % | L1 hit % | L2 hit % | smem bank conflicts "
+                     "| smem atomics (inst) | global RED (inst) | global atomics (inst) | top stalls |\n")
+            fh.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
             for k, r in kernels.items():
                 gb = (r.get("dram_bytes_per_launch") or 0) / 1e9
                 fh.write(f"| {k} | {r['duration_ms']:.3f} | {gb:.3f} | {r.get('dram_gbs', 0):.0f} | "
                          f"{(r['ipc'] or 0):.2f} | {(r['achieved_occupancy_pct'] or 0):.1f} | {(r['l1_hit_pct'] or 0):.1f} | "
                          f"{(r['l2_hit_pct'] or 0):.1f} | {r['smem_bank_conflicts']} | "
+                         f"{r['shared_atomic_instructions']} | {r['global_red_instructions']} | "
+                         f"{r['global_atomic_instructions']} | "
                          + ", ".join(f"{a}={b:.2f}" for a, b in r["top_stalls"]) + " |\n")
     print(json.dumps({k: {"ms": round(v["duration_ms"], 3), "dram_gb": round((v.get("dram_bytes_per_launch") or 0) / 1e9, 3)}
                       for k, v in kernels.items()}, indent=1))
