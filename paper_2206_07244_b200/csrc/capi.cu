@@ -423,6 +423,7 @@ struct spgemm_pipeline {
   int64_t* d_spill = nullptr;
   Spec spec{nullptr, nullptr, nullptr, 0};  // speculative numeric scratch (arena)
   bool regular_a = false;                    // A's longest row <= 4x its mean (set by setup)
+  bool reuse_route = false;                  // structure-reuse kernels (set by setup, see there)
   bool symbolic_only = false;                // spgemm_forecast_nnz: no speculative numeric, no C
   int32_t* d_blk = nullptr;
   int* d_flags = nullptr;
@@ -579,15 +580,21 @@ void spgemm_pipeline::setup() {
   const size_t o_spill = off;
   off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
   regular_a = M > 0 && static_cast<double>(h_sym.a_max_row) <= 4.0 * static_cast<double>(a_nnz) / static_cast<double>(M);
-  const bool use_spec = idx32 && M > 0 && avg_b_len > 8.0 && regular_a && M * kSpecCap * 12 <= kSpecBudget &&
+  // Structure-reuse route: A*A-shaped products of regular A with warp-sized A
+  // and B rows and B rows of > 8 entries on average (3-D stencils, FEM). The
+  // symbolic phase counts with k_sym_reuse, the numeric phase writes C with
+  // k_num_reuse -- no speculative scratch, no copy. SPGEMM_NO_REUSE=1 disables it.
+  reuse_route = idx32 && M > 0 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && regular_a &&
+                avg_b_len > 8.0 && square_like() && std::getenv("SPGEMM_NO_REUSE") == nullptr;
+  const bool use_spec = !reuse_route && idx32 && M > 0 && avg_b_len > 8.0 && regular_a &&
+                        M * kSpecCap * 12 <= kSpecBudget &&
                         !symbolic_only && std::getenv("SPGEMM_NO_SPEC") == nullptr;
   const size_t o_sflag = off, o_scol = align_up(o_sflag + (use_spec ? static_cast<size_t>(M) : 0), 256);
   const size_t o_sval = align_up(o_scol + (use_spec ? static_cast<size_t>(M) * kSpecCap * 4 : 0), 256);
   if (use_spec) off = align_up(o_sval + static_cast<size_t>(M) * kSpecCap * 8, 256);
   // the structure-reuse kernels' per-B-row shift flags (warp-sized A and B rows)
   // (only the speculative path's products -- regular A, long B rows -- reuse structure)
-  const bool use_shift = idx32 && M > 0 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && !symbolic_only &&
-                         regular_a && avg_b_len > 8.0 && square_like();
+  const bool use_shift = reuse_route;
   const size_t o_shift = off;
   if (use_shift) off = align_up(o_shift + static_cast<size_t>(std::max<int64_t>(b_rows, 1)), 256);
   arena_bytes = off;
@@ -657,6 +664,17 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
   } untag{ctx};
   const int64_t u = sym_plan.config.upper[bin];
   const bool g8 = avg_b_len <= kG8MaxBLen;
+  if (reuse_route && u > 32 && u <= 1024) {  // structure-reuse counting (kernels.cuh k_sym_reuse)
+    const size_t smem = static_cast<size_t>(kSymReuseWarps) * kSymReuseWarpBytes;
+    prepare_kernel(ctx, k_sym_reuse, smem);
+    const int rpw = reuse_rows_per_warp(ctx, k_sym_reuse, smem, rl.count);
+    const int grid = persistent_grid(ctx, k_sym_reuse, 32 * kSymReuseWarps, smem,
+                                     ceil_div(rl.count, kSymReuseWarps * rpw));
+    SPG_LAUNCH(ctx, "k_sym_reuse", s,
+               k_sym_reuse<<<grid, 32 * kSymReuseWarps, smem, s>>>(rl, A, B, d_rpt, scale, rpw, d_shift1,
+                                                                   d_info_sym));
+    return;
+  }
   auto group = [&](auto kern, int G, int T, int NGRP, int WB) {
     // Only where the numeric phase would also run a 32-lane group on a table
     // of 256 (rows with 513..1024 products, or 257..512 when B's rows average
@@ -916,7 +934,7 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
       // C = A*A of a regular matrix (stencils: the structure repeats row to
       // row): structure reuse; other products (the RAP chain's A*P, R*AP):
       // the dense-index kernel
-      if (spec.flag != nullptr && square_like()) {
+      if (reuse_route) {
         auto kern = &k_num_reuse<false>;
         const size_t smem = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
         prepare_kernel(ctx, kern, smem);

@@ -2422,6 +2422,130 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
   }
 }
 
+// Symbolic phase of the structure-reuse route (A*A-shaped products with
+// warp-sized A and B rows, e.g. 3-D stencils): nnz(C(i,:)) = nnz(C(i',:)) of
+// the warp's previous row i' whenever row i's structure is row i''s shifted
+// by d (the exact test of k_num_reuse: A-row lengths, entry-wise B-row lengths
+// and k_j(i) - k_j(i') = d; then either the per-B-row shift flags (d = 1) or a
+// per-product column check). Only rows that fail the test count their distinct
+// columns, with a 1024-slot table (a symbolic bin of <= 1024 products cannot
+// fill it). No values, no sort: the numeric phase (k_num_reuse) then writes C
+// in place -- no speculative scratch, no copy.
+constexpr int kSymReuseWarps = 8;
+constexpr int kSymReuseT = 1024;
+constexpr size_t kSymReuseWarpBytes = kSymReuseT * 4 + 2 * 32 * 16;
+__global__ void __launch_bounds__(32 * kSymReuseWarps)
+    k_sym_reuse(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale, int rows_per_warp,
+                const uint8_t* __restrict__ shift1, DevInfo* info) {
+  constexpr int G = 32;
+  const RowList rl = rl_in.resolved();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = smem_raw + static_cast<size_t>(warp) * kSymReuseWarpBytes;
+  int32_t* keys = reinterpret_cast<int32_t*>(wb);
+  EntryMeta* metab = reinterpret_cast<EntryMeta*>(wb + kSymReuseT * 4);
+  const uint32_t mult = scale * 0x9E3779B1u;
+  bool pvalid = false;
+  int pna = 0, mb = 0;
+  long long pn = 0;
+  int32_t pk = 0;
+  int plen = 0;
+  const int64_t R = rows_per_warp;
+  const int64_t first = (static_cast<int64_t>(blockIdx.x) * kSymReuseWarps + warp) * R;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kSymReuseWarps * R;
+  long long nreuse = 0, nfull = 0;
+  for (int64_t run0 = first; run0 < rl.count; run0 += stride) {
+    int64_t lrow = -1;
+    long long lnp = 0;
+    if (lane < R && run0 + lane < rl.count) {
+      lrow = rl.row(run0 + lane);
+      lnp = rpt[lrow];
+    }
+    unsigned todo = __ballot_sync(kFull, lnp != 0);  // no products: nnz 0 (pipeline.cpp:368-371)
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const int64_t row = __shfl_sync(kFull, lrow, src);
+      const long long np = __shfl_sync(kFull, lnp, src);
+      EntryMeta* meta = metab + mb * 32;
+      const EntryMeta* pmeta = metab + (mb ^ 1) * 32;
+      const int64_t a0 = A.rpt[row];
+      const int na = static_cast<int>(min(A.rpt[row + 1] - a0, static_cast<int64_t>(33)));
+      int len = 0;
+      int32_t k = 0;
+      if (lane < na) {
+        k = A.col[a0 + lane];
+        const int64_t r0 = B.rpt[k];
+        len = static_cast<int>(B.rpt[k + 1] - r0);
+        meta[lane] = EntryMeta{static_cast<int32_t>(r0), len, 0.0};
+      }
+      __syncwarp();
+      const int32_t d = __shfl_sync(kFull, k, 0) - __shfl_sync(kFull, pk, 0);
+      bool same = na <= G && pvalid && na == pna && __all_sync(kFull, lane >= na || (len == plen && k - pk == d));
+      if (same && !(d == 1 && shift1 != nullptr && __all_sync(kFull, lane >= na || shift1[k] != 0))) {
+        bool ok = true;
+        for (int j = 0; j < na && __all_sync(kFull, ok); ++j) {
+          const EntryMeta m = meta[j];
+          if (lane < m.len) ok = B.col[m.b0 + lane] - B.col[pmeta[j].b0 + lane] == d;
+        }
+        same = __all_sync(kFull, ok);
+      }
+      long long n;
+      if (same) {
+        n = pn;
+        ++nreuse;
+      } else {
+        // count the row's distinct columns (the table holds any row of these bins)
+        const int tsz = static_cast<int>(min(static_cast<long long>(kSymReuseT),
+                                             static_cast<long long>(1) << ceil_log2_ll(2 * np)));
+        const int lg = max(2, 31 - __clz(tsz));
+        const uint32_t hshift = 32u - static_cast<uint32_t>(lg), hmask = (1u << lg) - 1u;
+        fill_empty<G>(keys, 1 << lg, lane);
+        __syncwarp();
+        int cnt = 0;
+        for (int j = 0; j < min(na, G); ++j) {
+          const EntryMeta m = meta[j];
+          for (int q = lane; q < m.len; q += G) {
+            const int32_t c = B.col[m.b0 + q];
+            uint32_t h = (static_cast<uint32_t>(c) * mult) >> hshift;
+            int32_t cur = keys[h];
+            while (cur != c) {
+              if (cur == -1) {
+                cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, c);
+                if (cur == -1) {
+                  ++cnt;
+                  break;
+                }
+              } else {
+                h = (h + 1) & hmask;
+                cur = *reinterpret_cast<volatile int32_t*>(keys + h);
+              }
+            }
+          }
+        }
+        n = static_cast<long long>(__reduce_add_sync(kFull, static_cast<unsigned>(cnt)));
+        if (na > G) n = -1;  // (host-checked: A rows <= 32) never here
+        ++nfull;
+      }
+      if (lane == 0) {
+        rpt[row] = n;
+        if (n < 0) atomicOr(&info->error, kErrTableFull);
+      }
+      pvalid = na <= G;
+      pna = na;
+      pn = n;
+      pk = k;
+      plen = len;
+      mb ^= 1;
+      __syncwarp();
+    }
+  }
+  if (lane == 0 && (nreuse | nfull)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&info->reuse_rows), static_cast<unsigned long long>(nreuse));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&info->full_rows), static_cast<unsigned long long>(nfull));
+  }
+}
+
 // shift1[k] = 1 when B row k is B row k-1 shifted by one column (same length,
 // every column one larger): the per-B-row precondition that lets k_num_reuse
 // accept a row adjacent to its predecessor (d = 1) without comparing every
