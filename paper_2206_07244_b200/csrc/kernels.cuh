@@ -2233,9 +2233,6 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
     bool reuse = pvalid && na == pna && (SPEC || n == pn) &&
                  __all_sync(kFull, lane >= na || (len == plen && k - pk == d));
     if (reuse) {
-      double2* v2 = reinterpret_cast<double2*>(vals);
-      for (int s = lane; s < (pn + 1) / 2; s += G) v2[s] = make_double2(0.0, 0.0);
-      __syncwarp();
       bool ok = true;
       if (d == 1 && shift1 != nullptr && __all_sync(kFull, lane >= na || shift1[k] != 0)) {
         // every B row of the row is its predecessor shifted by one column
@@ -2257,11 +2254,15 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
             const bool on = j < na && lane < m.len;
             av[u] = m.av;
             bv[u] = on ? bval[m.b0] : 0.0;
-            pos[u] = on ? mapl[j * G] : NMAX;
+            // low 7 bits: the position (NMAX: the spare slot); bit 8: first product
+            const int pm = on ? mapl[j * G] : 0x80;
+            pos[u] = on ? (pm & 0x7f) | ((pm & 0x80) << 1) : NMAX | 0x100;
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            vals[pos[u]] = __dadd_rn(vals[pos[u]], __dmul_rn(av[u], bv[u]));
+            const int pu = pos[u] & 0xff;
+            const double prev = (pos[u] & 0x100) ? 0.0 : vals[pu];
+            vals[pu] = __dadd_rn(prev, __dmul_rn(av[u], bv[u]));
             __syncwarp();
           }
         }
@@ -2273,8 +2274,9 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
             const int32_t cp = B.col[pmeta[j].b0 + lane];
             const double x = __dmul_rn(m.av, B.val[m.b0 + lane]);
             ok = ok && c - cp == d;
-            const int pos = map[j * G + lane];
-            vals[pos] = __dadd_rn(vals[pos], x);
+            const int pm = map[j * G + lane];
+            const int pos = pm & 0x7f;
+            vals[pos] = __dadd_rn((pm & 0x80) ? 0.0 : vals[pos], x);
           }
           if (!__all_sync(kFull, ok)) break;  // structure differs: stop early (the full path recomputes)
         }
@@ -2396,9 +2398,20 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
       rank[ix] = static_cast<uint8_t>(e);
     }
     __syncwarp();
-    // product -> output position for the next row
+    // product -> output position for the next row, bit 7 set on the first
+    // product (in A order) of its position: the reuse path writes 0.0 + x
+    // there instead of reading a zeroed accumulator
+    uint8_t* seen = reinterpret_cast<uint8_t*>(cols);  // (the claim-order columns are consumed)
+    for (int e = lane; e < NMAX; e += G) seen[e] = 0;
+    __syncwarp();
     for (int j = 0; j < na; ++j) {
-      if (lane < __shfl_sync(kFull, len, j)) map[j * G + lane] = rank[map[j * G + lane]];
+      if (lane < __shfl_sync(kFull, len, j)) {
+        const int p = rank[map[j * G + lane]];
+        const int first = seen[p] == 0 ? 0x80 : 0;
+        seen[p] = 1;
+        map[j * G + lane] = static_cast<uint8_t>(p | first);
+      }
+      __syncwarp();
     }
     if constexpr (SPEC) {
       if (lane == 0) {

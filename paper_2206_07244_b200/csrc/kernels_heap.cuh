@@ -66,6 +66,25 @@ constexpr size_t kBigNumSmem = sizeof(uint32_t) * kBigWordsPad + sizeof(uint16_t
                                sizeof(uint32_t) * (kBigWords / kBigSuper) + sizeof(BigTile);
 static_assert(kBigNumSmem <= 227 * 1024, "heap-tier numeric block exceeds the opt-in shared memory");
 
+// B's entries stream through L2 once per pass: loaded with an evict-first
+// policy, so they do not push out the C.val lines of the rows in flight
+// (which the ordered heap kernel read-modify-writes, evict-last).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int32_t ld_first(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_first(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 // Walks every product of A row [a0, a1): visit(col, x, valid) is called by all
 // 32 lanes of every warp once per round (valid = the lane holds a product).
 // Round mapping: lane l of a round starting at product p0 belongs to entry
@@ -76,6 +95,7 @@ __device__ __forceinline__ void big_walk(const DevCsr& A, const DevCsr& B, int64
                                          F visit) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr long long kLimit = (1ll << 31) - 1;
+  const uint64_t once = l2_evict_first_policy();
   for (int64_t e0 = a0; e0 < a1; e0 += t.ne) {
     const int ne = static_cast<int>(min(static_cast<int64_t>(kBigThreads), a1 - e0));
     long long len = 0;
@@ -135,15 +155,15 @@ __device__ __forceinline__ void big_walk(const DevCsr& A, const DevCsr& B, int64
             double bv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              c[u] = B.col[bj + p0 + 32 * u + lane];
-              if constexpr (VALS) bv[u] = B.val[bj + p0 + 32 * u + lane];
+              c[u] = ld_first(B.col + bj + p0 + 32 * u + lane, once);
+              if constexpr (VALS) bv[u] = ld_first(B.val + bj + p0 + 32 * u + lane, once);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) visit(c[u], VALS ? __dmul_rn(a, bv[u]) : 0.0, true);
           }
           for (; p0 + 32 <= stop; p0 += 32) {
             const int32_t at = bj + p0 + lane;
-            visit(B.col[at], VALS ? __dmul_rn(a, B.val[at]) : 0.0, true);
+            visit(ld_first(B.col + at, once), VALS ? __dmul_rn(a, ld_first(B.val + at, once)) : 0.0, true);
           }
           if (p0 >= pw1) break;
           if (p0 == send) {
@@ -162,8 +182,8 @@ __device__ __forceinline__ void big_walk(const DevCsr& A, const DevCsr& B, int64
         double x = 0.0;
         if (valid) {
           const int32_t at = t.b0[j] + (p - t.S[j]);
-          col = B.col[at];
-          if constexpr (VALS) x = __dmul_rn(t.av[j], B.val[at]);
+          col = ld_first(B.col + at, once);
+          if constexpr (VALS) x = __dmul_rn(t.av[j], ld_first(B.val + at, once));
         }
         visit(col, x, valid);
         // next round starts at p0+32: the entry holding it
@@ -435,6 +455,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
                                            sizeof(uint16_t) * kBigPrePad + sizeof(uint32_t) * (kBigWords / kBigSuper));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t keep = l2_evict_last_policy();  // the rows' C.val stays in L2 between its RMWs
+  const uint64_t once = l2_evict_first_policy();  // B's entries stream through
   for (int64_t idx = blockIdx.x; idx < rl.count; idx += gridDim.x) {
     const int64_t row = rl.row(idx);
     const int64_t base = rpt[row];
@@ -516,8 +537,8 @@ __global__ void __launch_bounds__(kBigThreads, 1)
               int32_t col = 0;
               double bv = 0.0;
               if (q < lj) {
-                col = B.col[sj + q];
-                bv = B.val[sj + q];
+                col = ld_first(B.col + sj + q, once);
+                bv = ld_first(B.val + sj + q, once);
               }
               const uint32_t off = static_cast<uint32_t>(col - c0);
               in[u] = q < lj && off < static_cast<uint32_t>(kBigWindow);
