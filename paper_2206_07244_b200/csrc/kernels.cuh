@@ -2180,12 +2180,22 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
   long long nreuse = 0, nfull = 0;  // rows through each path (DevInfo counters)
   for (int64_t run0 = first; run0 < rl.count; run0 += stride) {
    // the run's row ids and skip tests, 32 at a time; then its rows in order
-   int64_t lrow = -1;
+   // the run's row ids, skip tests, C offsets / nprod and A-row bounds, one row per lane
+   int64_t lrow = -1, lbase = 0, lnext = 0, la0 = 0, la1 = 0;
    bool need = false;
    if (lane < R && run0 + lane < rl.count) {
      lrow = rl.row(run0 + lane);
-     if constexpr (SPEC) need = rpt[lrow] != 0;  // no products: the symbolic kernel writes the 0
-     else need = !sp.done(lrow);                 // rows done speculatively are copied by k_spec_copy
+     lbase = rpt[lrow];
+     if constexpr (SPEC) {
+       need = lbase != 0;  // no products: the symbolic kernel writes the 0
+     } else {
+       lnext = rpt[lrow + 1];
+       need = !sp.done(lrow) && lnext > lbase;  // done speculatively (k_spec_copy) or empty
+     }
+     if (need) {
+       la0 = A.rpt[lrow];
+       la1 = A.rpt[lrow + 1];
+     }
    }
    unsigned todo = __ballot_sync(kFull, need);
    while (todo) {
@@ -2196,20 +2206,17 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
     int n = 0;
     long long bound;
     if constexpr (SPEC) {
-      const long long np = rpt[row];
-      if (np == 0) continue;  // no products: the symbolic kernel writes the 0
+      const long long np = __shfl_sync(kFull, lbase, src);
       bound = min(np, static_cast<long long>(NMAX));
     } else {
-      if (sp.done(row)) continue;  // computed in the symbolic phase, copied by k_spec_copy
-      base = rpt[row];
-      n = static_cast<int>(rpt[row + 1] - base);
-      if (n == 0) continue;
+      base = __shfl_sync(kFull, lbase, src);
+      n = static_cast<int>(__shfl_sync(kFull, lnext, src) - base);
       bound = n;
     }
     EntryMeta* meta = metab + mb * 32;
     const EntryMeta* pmeta = metab + (mb ^ 1) * 32;
-    const int64_t a0 = A.rpt[row];
-    const int na = static_cast<int>(min(A.rpt[row + 1] - a0, static_cast<int64_t>(33)));
+    const int64_t a0 = __shfl_sync(kFull, la0, src);
+    const int na = static_cast<int>(min(__shfl_sync(kFull, la1, src) - a0, static_cast<int64_t>(33)));
     int len = 0;
     int32_t k = 0;
     double av = 0.0;
@@ -2468,11 +2475,14 @@ __global__ void __launch_bounds__(32 * kSymReuseWarps)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kSymReuseWarps * R;
   long long nreuse = 0, nfull = 0;
   for (int64_t run0 = first; run0 < rl.count; run0 += stride) {
-    int64_t lrow = -1;
+    // the run's row ids, nprod and A-row bounds, one row per lane
+    int64_t lrow = -1, la0 = 0, la1 = 0;
     long long lnp = 0;
     if (lane < R && run0 + lane < rl.count) {
       lrow = rl.row(run0 + lane);
       lnp = rpt[lrow];
+      la0 = A.rpt[lrow];
+      la1 = A.rpt[lrow + 1];
     }
     unsigned todo = __ballot_sync(kFull, lnp != 0);  // no products: nnz 0 (pipeline.cpp:368-371)
     while (todo) {
@@ -2482,8 +2492,8 @@ __global__ void __launch_bounds__(32 * kSymReuseWarps)
       const long long np = __shfl_sync(kFull, lnp, src);
       EntryMeta* meta = metab + mb * 32;
       const EntryMeta* pmeta = metab + (mb ^ 1) * 32;
-      const int64_t a0 = A.rpt[row];
-      const int na = static_cast<int>(min(A.rpt[row + 1] - a0, static_cast<int64_t>(33)));
+      const int64_t a0 = __shfl_sync(kFull, la0, src);
+      const int na = static_cast<int>(min(__shfl_sync(kFull, la1, src) - a0, static_cast<int64_t>(33)));
       int len = 0;
       int32_t k = 0;
       if (lane < na) {
