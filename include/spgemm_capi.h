@@ -277,6 +277,14 @@ spgemm_status spgemm_forecast_nnz_multi(spgemm_ctx** ctxs, int32_t n, const spge
                                         int64_t* row_bounds, int64_t* total_nnz, int64_t* total_nprod);
 
 /* ----------------------------------------------- standalone GPU kernels */
+/* csr_from_coo() (csr.cpp:12-72) on the device:
+ * n triples (row, col, val) in input order -- host arrays, or device arrays
+ * when on_device -- to a device CSR with each row's columns sorted and
+ * duplicates summed in input order (the first as is, then +=). Errors as the
+ * reference: negative shape, column count beyond 32 bits, an entry outside the
+ * shape (INVALID_ARGUMENT with the reference's message). */
+spgemm_status spgemm_csr_from_coo(spgemm_ctx* ctx, int64_t rows, int64_t cols, int64_t n, const int64_t* row,
+                                  const int64_t* col, const double* val, int32_t on_device, spgemm_matrix** out);
 /* compute_nprod() (reference.cpp:37-55) on the device: out[M] host or device. */
 spgemm_status spgemm_compute_nprod(spgemm_ctx* ctx, const spgemm_csr_view* a,
                                    const spgemm_csr_view* b, int64_t* out_host,

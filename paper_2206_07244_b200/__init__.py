@@ -4,7 +4,7 @@ The product is the sm_100a library ``lib/libspgemm_b200.so`` behind the C ABI in
 ``include/spgemm_capi.h``; :mod:`.api` mirrors the reference's C++ API on top of it.
 """
 from .api import (  # noqa: F401
-    AllocStats, BinConfig, BinningResult, BinStrategy, Context, CsrMatrix, CudaError, DeviceMatrix,
+    AllocStats, BinConfig, csr_from_coo_device, BinningResult, BinStrategy, Context, CsrMatrix, CudaError, DeviceMatrix,
     ExecutionPlan, InvalidArgument, LogicError, MatrixStats, NnzForecast, NoDevice, SpgemmOptions, SpgemmOutput,
     SpgemmPipeline, StepTimings, SYMBOLIC, NUMERIC, build_rpt, classify, compute_nprod, forecast_nnz,
     forecast_nnz_multi, get_context,

@@ -124,6 +124,7 @@ _decl("spgemm_matrix_download", _st, [_P, _P, _P, _P, _P])
 _decl("spgemm_matrix_free", None, [_P])
 _decl("spgemm_matrix_as_operand", _st, [_P, C.POINTER(CsrView)])
 _decl("spgemm_ctx_trim", _st, [_P, C.c_uint64])
+_decl("spgemm_csr_from_coo", _st, [_P, C.c_int64, C.c_int64, C.c_int64, _P, _P, _P, C.c_int32, C.POINTER(_P)])
 _decl("spgemm_ctx_wait_stream", _st, [_P, _P])
 _decl("spgemm_matrix_checksum", _st, [_P, _P, C.c_int64, C.c_int64, _P, _P])
 _decl("spgemm_matrix_download_async", _st, [_P, _P, _P, _P, _P, C.c_int32])
@@ -154,6 +155,7 @@ EXPORTED = [
     "spgemm_matrix_download_async", "spgemm_ctx_wait_downloads", "spgemm_multiply_multi",
     "spgemm_matrices_download_stitched", "spgemm_compute_nprod", "spgemm_forecast_nnz", "spgemm_forecast_nnz_multi",
     "spgemm_multiply_into", "spgemm_matrix_as_operand", "spgemm_ctx_wait_stream", "spgemm_ctx_trim",
+    "spgemm_csr_from_coo",
     "spgemm_build_rpt", "spgemm_run_binning",
 ]
 

@@ -898,6 +898,34 @@ def forecast_nnz_multi(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptio
     return NnzForecast(a.rows, int(tn.value), int(tp.value), rows, [int(x) for x in bounds])
 
 
+def csr_from_coo_device(rows: int, cols: int, row, col, val, device: Optional[int] = None) -> "DeviceMatrix":
+    """csr.cpp:12-72 (csr_from_coo) on the device: triples in input order (numpy
+    arrays or torch CUDA tensors) -> a device CSR with each row's columns sorted
+    and duplicates summed in input order. Raises IndexError for an entry outside
+    the shape and InvalidArgument for a bad shape, like the reference."""
+    ctx = get_context(device)
+    if _is_torch_cuda(row):
+        import torch
+        r, c, v = (t.contiguous() for t in (row.to(torch.int64), col.to(torch.int64), val.to(torch.float64)))
+        ptrs, on_dev, keep = (r.data_ptr(), c.data_ptr(), v.data_ptr()), 1, (r, c, v)
+        _order_device_operands(ctx)
+    else:
+        r = np.ascontiguousarray(row, np.int64)
+        c = np.ascontiguousarray(col, np.int64)
+        v = np.ascontiguousarray(val, np.float64)
+        if not (r.size == c.size == v.size):
+            raise InvalidArgument("csr_from_coo: row/col/val lengths differ")
+        ptrs, on_dev, keep = (r.ctypes.data, c.ctypes.data, v.ctypes.data), 0, (r, c, v)
+    n = int(keep[0].numel() if on_dev else keep[0].size)
+    h = C.c_void_p()
+    st = _c.lib.spgemm_csr_from_coo(ctx.handle, int(rows), int(cols), n, *(p if n else None for p in ptrs), on_dev,
+                                    C.byref(h))
+    if st != _c.OK and "outside" in _c.last_error():
+        raise IndexError(_c.last_error())
+    _check(st)
+    return DeviceMatrix(h, ctx)
+
+
 def multiply_device(a: CsrMatrix, b: CsrMatrix, options: Optional[SpgemmOptions] = None,
                     device: Optional[int] = None):
     """C = A*B with C left in HBM. Returns (DeviceMatrix, SpgemmOutput with c=None)."""

@@ -18,7 +18,7 @@ SOURCES = [os.path.join(CSRC, "capi.cu")]
 CXX_SOURCES = [os.path.join(CSRC, "cxx_api.cpp"), os.path.join(CSRC, "multi.cpp")]  # the reference's C++ API over the C ABI
 HEADERS = [os.path.join(ROOT, "include", "spgemm_capi.h")] + [
     os.path.join(ROOT, "include", "spgemm", h) for h in sorted(os.listdir(os.path.join(ROOT, "include", "spgemm")))]
-DEPS = SOURCES + CXX_SOURCES + HEADERS + [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "kernels_heap.cuh")]
+DEPS = SOURCES + CXX_SOURCES + HEADERS + [os.path.join(CSRC, h) for h in ("kernels.cuh", "kernels_heap.cuh", "kernels_coo.cuh")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

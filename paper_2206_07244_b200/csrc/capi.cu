@@ -28,6 +28,7 @@
 
 #include "kernels.cuh"
 #include "kernels_heap.cuh"
+#include "kernels_coo.cuh"
 #include "spgemm_capi.h"
 
 using namespace spgemm_b200;
@@ -1796,6 +1797,130 @@ spgemm_status spgemm_forecast_nnz(spgemm_ctx* ctx, const spgemm_csr_view* a, con
   spgemm_pipeline_destroy(p);
   g_err = keep;
   return st;
+}
+
+// csr_from_coo (csr.cpp:12-72) on the device (kernels_coo.cuh).
+spgemm_status spgemm_csr_from_coo(spgemm_ctx* ctx, int64_t rows, int64_t cols, int64_t n, const int64_t* row,
+                                  const int64_t* col, const double* val, int32_t on_device, spgemm_matrix** out) {
+  return guard([&] {
+    if (!ctx || !out) fail(SPGEMM_INVALID_ARGUMENT, "csr_from_coo: null argument");
+    *out = nullptr;
+    if (rows < 0 || cols < 0) fail(SPGEMM_INVALID_ARGUMENT, "csr_from_coo: negative matrix shape");
+    if (cols > std::numeric_limits<int32_t>::max())
+      fail(SPGEMM_INVALID_ARGUMENT, "csr_from_coo: column count exceeds 32-bit index range");
+    if (n < 0 || n >= (int64_t(1) << 32)) fail(SPGEMM_INVALID_ARGUMENT, "csr_from_coo: entry count out of range");
+    if (n > 0 && (!row || !col || !val)) fail(SPGEMM_INVALID_ARGUMENT, "csr_from_coo: null triples");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = ctx->main_s;
+    std::vector<void*> tmp;
+    auto scratch = [&](size_t bytes) {
+      void* p = dev_alloc(bytes, s);
+      tmp.push_back(p);
+      return p;
+    };
+    struct Cleanup {
+      std::vector<void*>* t;
+      cudaStream_t s;
+      ~Cleanup() {
+        for (void* p : *t) dev_free(p, s);
+      }
+    } cleanup{&tmp, s};
+    const int64_t* drow = row;
+    const int64_t* dcol = col;
+    const double* dval = val;
+    if (!on_device && n > 0) {
+      auto* r = static_cast<int64_t*>(scratch(static_cast<size_t>(n) * 8));
+      auto* c = static_cast<int64_t*>(scratch(static_cast<size_t>(n) * 8));
+      auto* v = static_cast<double*>(scratch(static_cast<size_t>(n) * 8));
+      ck(cudaMemcpyAsync(r, row, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, s), "H2D row");
+      ck(cudaMemcpyAsync(c, col, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, s), "H2D col");
+      ck(cudaMemcpyAsync(v, val, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, s), "H2D val");
+      drow = r;
+      dcol = c;
+      dval = v;
+    } else if (on_device) {
+      cudaEvent_t e = pooled_event(ctx);
+      ck(cudaEventRecord(e, cudaStreamLegacy), "record default stream");
+      ck(cudaStreamWaitEvent(s, e, 0), "wait default stream");
+      ctx->ev_pool.push_back(e);
+    }
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, ceil_div(n, 256))));
+    // shape check: the first offending entry, reported like the reference
+    auto* bad = static_cast<unsigned long long*>(scratch(8));
+    ck(cudaMemsetAsync(bad, 0xff, 8, s), "memset");
+    if (n > 0) {
+      SPG_LAUNCH(ctx, "k_coo_check", s, k_coo_check<<<grid, 256, 0, s>>>(drow, dcol, n, rows, cols, bad));
+    }
+    unsigned long long hbad = ~0ull;
+    ck(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (hbad != ~0ull) {
+      int64_t br = 0, bc = 0;
+      ck(cudaMemcpy(&br, drow + hbad, 8, cudaMemcpyDeviceToHost), "D2H");
+      ck(cudaMemcpy(&bc, dcol + hbad, 8, cudaMemcpyDeviceToHost), "D2H");
+      fail(SPGEMM_INVALID_ARGUMENT, "csr_from_coo: entry (" + std::to_string(br) + ", " + std::to_string(bc) +
+                                        ") outside " + std::to_string(rows) + "x" + std::to_string(cols) + " shape");
+    }
+    // two stable counting sorts: by column, then by row
+    auto* perm_a = static_cast<uint32_t*>(scratch(static_cast<size_t>(std::max<int64_t>(n, 1)) * 4));
+    auto* perm_b = static_cast<uint32_t*>(scratch(static_cast<size_t>(std::max<int64_t>(n, 1)) * 4));
+    const int64_t ntile = ceil_div(n, kCooTile);
+    auto* done = static_cast<int*>(scratch(static_cast<size_t>(std::max<int64_t>(ntile, 1)) * 4 + 64));
+    auto* info = static_cast<DevInfo*>(scratch(sizeof(DevInfo)));
+    auto scan = [&](int64_t* data, int64_t len) {  // exclusive, in place
+      const int64_t nt = ceil_div(len, kScanTile);
+      auto* flags = static_cast<int*>(scratch(static_cast<size_t>(nt) * 4));
+      auto* sums = static_cast<long long*>(scratch(static_cast<size_t>(nt) * 16));
+      ck(cudaMemsetAsync(flags, 0, static_cast<size_t>(nt) * 4, s), "memset");
+      ck(cudaMemsetAsync(info, 0, sizeof(DevInfo), s), "memset");
+      SPG_LAUNCH(ctx, "k_scan", s,
+                 k_scan<<<static_cast<unsigned>(nt), kScanThreads, 0, s>>>(data, len, flags, sums, sums + nt, info));
+    };
+    auto pass = [&](const int64_t* key, int64_t nkeys, const uint32_t* pin, uint32_t* pout) {
+      auto* cnt = static_cast<int64_t*>(scratch(static_cast<size_t>(nkeys + 1) * 8));
+      ck(cudaMemsetAsync(cnt, 0, static_cast<size_t>(nkeys + 1) * 8, s), "memset");
+      SPG_LAUNCH(ctx, "k_coo_count", s,
+                 k_coo_count<<<grid, 256, 0, s>>>(key, n, reinterpret_cast<unsigned long long*>(cnt)));
+      scan(cnt, nkeys + 1);
+      ck(cudaMemsetAsync(done, 0, static_cast<size_t>(ntile) * 4 + 64, s), "memset");
+      int* tiles = done + ntile;
+      SPG_LAUNCH(ctx, "k_coo_scatter", s,
+                 k_coo_scatter<<<static_cast<unsigned>(ntile), kCooThreads, 0, s>>>(
+                     key, pin, n, reinterpret_cast<long long*>(cnt), done, tiles, pout));
+    };
+    auto* m = new spgemm_matrix();
+    m->ctx = ctx;
+    m->rows = rows;
+    m->cols = cols;
+    try {
+      m->rpt = static_cast<int64_t*>(dev_alloc(static_cast<size_t>(rows + 1) * 8, s));
+      ck(cudaMemsetAsync(m->rpt, 0, static_cast<size_t>(rows + 1) * 8, s), "memset");
+      int64_t nnz = 0;
+      if (n > 0) {
+        pass(dcol, cols, nullptr, perm_a);
+        pass(drow, rows, perm_a, perm_b);
+        auto* head = static_cast<int64_t*>(scratch(static_cast<size_t>(n + 1) * 8));
+        ck(cudaMemsetAsync(head + n, 0, 8, s), "memset");
+        SPG_LAUNCH(ctx, "k_coo_heads", s,
+                   k_coo_heads<<<grid, 256, 0, s>>>(drow, dcol, perm_b, n, head,
+                                                   reinterpret_cast<unsigned long long*>(m->rpt)));
+        scan(head, n + 1);  // head -> compacted index of each run head; total = nnz
+        scan(m->rpt, rows + 1);
+        ck(cudaMemcpyAsync(&nnz, head + n, 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+        m->col = static_cast<int32_t*>(dev_alloc(static_cast<size_t>(std::max<int64_t>(nnz, 1)) * 4, s));
+        m->val = static_cast<double*>(dev_alloc(static_cast<size_t>(std::max<int64_t>(nnz, 1)) * 8, s));
+        SPG_LAUNCH(ctx, "k_coo_fold", s,
+                   k_coo_fold<<<grid, 256, 0, s>>>(drow, dcol, dval, perm_b, n, head, m->col, m->val));
+      }
+      m->nnz = nnz;
+      ck(cudaStreamSynchronize(s), "sync");
+    } catch (...) {
+      spgemm_matrix_free(m);
+      throw;
+    }
+    *out = m;
+  });
 }
 
 spgemm_status spgemm_build_rpt(spgemm_ctx* ctx, int64_t* values, int64_t n, int64_t* total) {

@@ -203,3 +203,13 @@ def read_matrix_market_csr(path: str) -> CsrMatrix:
     from .synthetic import csr_from_coo
     coo = read_matrix_market(path)
     return csr_from_coo(coo.rows, coo.cols, coo.row, coo.col, coo.value)
+
+
+def read_matrix_market_device(path: str, device=None):
+    """read_matrix_market_csr with the CSR assembled on the device: the file is
+    parsed on the host (text I/O), the triples are sorted, folded (duplicates
+    summed in input order) and compacted by the sm_100a kernels
+    (api.csr_from_coo_device). Returns a DeviceMatrix."""
+    from .api import csr_from_coo_device
+    coo = read_matrix_market(path)
+    return csr_from_coo_device(coo.rows, coo.cols, coo.row, coo.col, coo.value, device=device)
