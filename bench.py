@@ -236,7 +236,7 @@ def run_reference(args):
     else:
         mats = list(S.config_matrices(args.config))
     a = mats[0]
-    frac = {1: 1.0, 2: 1.0, 3: 0.02, 4: 1.0, 5: 0.0005}[args.config]
+    frac = {1: 1.0, 2: 1.0, 3: 0.02, 4: 1.0, 5: 0.0005 if args.rmat_scale >= 24 else 0.0002}[args.config]
     r0 = int(a.rows * (0.5 - frac / 2)) if frac < 1 else 0
     r1 = r0 + int(a.rows * frac) if frac < 1 else a.rows
     if frac < 1:
