@@ -668,12 +668,10 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
   if (reuse_route && u > 32 && u <= 1024) {  // structure-reuse counting (kernels.cuh k_sym_reuse)
     const size_t smem = static_cast<size_t>(kSymReuseWarps) * kSymReuseWarpBytes;
     prepare_kernel(ctx, k_sym_reuse, smem);
-    const int rpw = reuse_rows_per_warp(ctx, k_sym_reuse, smem, rl.count);
-    const int grid = persistent_grid(ctx, k_sym_reuse, 32 * kSymReuseWarps, smem,
-                                     ceil_div(rl.count, kSymReuseWarps * rpw));
+    // (the bin's size is on the device: the kernel sizes its runs from it)
+    const int grid = persistent_grid(ctx, k_sym_reuse, 32 * kSymReuseWarps, smem, ceil_div(rl.count, kSymReuseWarps));
     SPG_LAUNCH(ctx, "k_sym_reuse", s,
-               k_sym_reuse<<<grid, 32 * kSymReuseWarps, smem, s>>>(rl, A, B, d_rpt, scale, rpw, d_shift1,
-                                                                   d_info_sym));
+               k_sym_reuse<<<grid, 32 * kSymReuseWarps, smem, s>>>(rl, A, B, d_rpt, scale, 0, d_shift1, d_info_sym));
     return;
   }
   auto group = [&](auto kern, int G, int T, int NGRP, int WB) {
@@ -689,8 +687,8 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
         auto sk = &k_num_reuse<true>;
         const size_t ssm = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
         prepare_kernel(ctx, sk, ssm);
-        const int rpw = reuse_rows_per_warp(ctx, sk, ssm, rl.count);
-        const int sgrid = persistent_grid(ctx, sk, 32 * kReuseWarps, ssm, ceil_div(rl.count, kReuseWarps * rpw));
+        const int rpw = 0;  // (the symbolic bin's size is on the device: the kernel sizes its runs)
+        const int sgrid = persistent_grid(ctx, sk, 32 * kReuseWarps, ssm, ceil_div(rl.count, kReuseWarps));
         SPG_LAUNCH(ctx, "k_num_reuse<spec>", s,
                    sk<<<sgrid, 32 * kReuseWarps, ssm, s>>>(rl, A, B, d_rpt, nullptr, nullptr, scale, d_info_sym,
                                                            spec, rpw, d_shift1));

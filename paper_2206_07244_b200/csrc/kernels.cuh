@@ -2173,8 +2173,15 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
   int pna = 0, pn = 0, mb = 0;
   int32_t pk = 0;
   int plen = 0;
-  // runs of rows_per_warp (<= kReuseRows) consecutive rows per warp per sweep
-  const int64_t R = rows_per_warp;
+  // runs of R (<= kReuseRows, a power of two) consecutive rows per warp per
+  // sweep: as many as keep every warp busy, from the bin's size read on the
+  // device (rows_per_warp > 0 overrides)
+  int64_t R = rows_per_warp;
+  if (R <= 0) {
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * kReuseWarps;
+    R = kReuseRows;
+    while (R > 1 && rl.count < warps * R) R >>= 1;
+  }
   const int64_t first = (static_cast<int64_t>(blockIdx.x) * kReuseWarps + warp) * R;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kReuseWarps * R;
   long long nreuse = 0, nfull = 0;  // rows through each path (DevInfo counters)
@@ -2457,112 +2464,155 @@ constexpr size_t kSymReuseWarpBytes = kSymReuseT * 4 + 2 * 32 * 16;
 __global__ void __launch_bounds__(32 * kSymReuseWarps)
     k_sym_reuse(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale, int rows_per_warp,
                 const uint8_t* __restrict__ shift1, DevInfo* info) {
+  // A warp takes runs of 32 consecutive rows of the bin, one row per lane:
+  // every lane tests ITS row against the row before it in the bin (lane - 1;
+  // lane 0: the previous run's last row) -- all 32 tests at once, the loads of
+  // different rows independent. Exact test for d = 1: equal A-row length,
+  // k_j(i) - k_j(i-1) = 1 and equal B-row lengths for every entry, and the
+  // per-B-row shift flag of every k_j(i). A row that passes has its
+  // predecessor's count; the others ("heads") count their distinct columns,
+  // warp-cooperatively, and the counts are copied forward lane to lane.
   constexpr int G = 32;
   const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wb = smem_raw + static_cast<size_t>(warp) * kSymReuseWarpBytes;
   int32_t* keys = reinterpret_cast<int32_t*>(wb);
-  EntryMeta* metab = reinterpret_cast<EntryMeta*>(wb + kSymReuseT * 4);
   const uint32_t mult = scale * 0x9E3779B1u;
-  bool pvalid = false;
-  int pna = 0, mb = 0;
-  long long pn = 0;
-  int32_t pk = 0;
-  int plen = 0;
-  const int64_t R = rows_per_warp;
+  // runs of R consecutive bin rows per warp, taken in pieces of min(R, 32);
+  // the count carries over between the pieces. R follows the bin's size (read
+  // on the device): 32*S rows (S <= 8) while every warp stays busy, shorter
+  // runs for small bins. (rows_per_warp > 0 overrides.)
+  int64_t R = rows_per_warp;
+  if (R <= 0) {
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * kSymReuseWarps;
+    R = 32 * max(1ll, min(8ll, static_cast<long long>(rl.count / (warps * 32))));
+    while (R > 4 && rl.count < warps * R) R >>= 1;
+  }
+  bool cvalid = false;  // the previous piece's last row (warp-uniform)
+  int64_t c_a0 = 0;
+  int c_na = 0;
+  long long c_n = 0;
+  long long nreuse = 0, nfull = 0;
   const int64_t first = (static_cast<int64_t>(blockIdx.x) * kSymReuseWarps + warp) * R;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kSymReuseWarps * R;
-  long long nreuse = 0, nfull = 0;
-  for (int64_t run0 = first; run0 < rl.count; run0 += stride) {
-    // the run's row ids, nprod and A-row bounds, one row per lane
-    int64_t lrow = -1, la0 = 0, la1 = 0;
-    long long lnp = 0;
-    if (lane < R && run0 + lane < rl.count) {
-      lrow = rl.row(run0 + lane);
-      lnp = rpt[lrow];
-      la0 = A.rpt[lrow];
-      la1 = A.rpt[lrow + 1];
+  const int P = static_cast<int>(min(static_cast<int64_t>(G), R));  // rows per piece (R: a multiple of P)
+  for (int64_t run0 = first; run0 < rl.count; run0 += (run0 - first) % R + P >= R ? stride - (R - P) : P) {
+    if ((run0 - first) % R == 0) cvalid = false;  // a new run: its first row is a head
+    const bool valid = lane < P && run0 + lane < rl.count;
+    int64_t row = 0, a0 = 0;
+    long long np = 0;
+    int na = 0;
+    if (valid) {
+      row = rl.row(run0 + lane);
+      np = rpt[row];
+      a0 = A.rpt[row];
+      na = static_cast<int>(A.rpt[row + 1] - a0);
     }
-    unsigned todo = __ballot_sync(kFull, lnp != 0);  // no products: nnz 0 (pipeline.cpp:368-371)
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1u;
-      const int64_t row = __shfl_sync(kFull, lrow, src);
-      const long long np = __shfl_sync(kFull, lnp, src);
-      EntryMeta* meta = metab + mb * 32;
-      const EntryMeta* pmeta = metab + (mb ^ 1) * 32;
-      const int64_t a0 = __shfl_sync(kFull, la0, src);
-      const int na = static_cast<int>(min(__shfl_sync(kFull, la1, src) - a0, static_cast<int64_t>(33)));
-      int len = 0;
-      int32_t k = 0;
-      if (lane < na) {
-        k = A.col[a0 + lane];
-        const int64_t r0 = B.rpt[k];
-        len = static_cast<int>(B.rpt[k + 1] - r0);
-        meta[lane] = EntryMeta{static_cast<int32_t>(r0), len, 0.0};
+    // the predecessor in the bin: lane - 1, or the previous run's last row
+    int64_t p_a0 = __shfl_up_sync(kFull, a0, 1);
+    int p_na = __shfl_up_sync(kFull, na, 1);
+    bool p_ok = __shfl_up_sync(kFull, valid && np != 0, 1);
+    if (lane == 0) {
+      p_a0 = c_a0;
+      p_na = c_na;
+      p_ok = cvalid;
+    }
+    bool same = valid && np != 0 && p_ok && na == p_na && na <= G && shift1 != nullptr;
+    // 8 entries per round, all their loads issued before any is tested
+    for (int j0 = 0; __any_sync(kFull, same && j0 < na); j0 += 8) {
+      int32_t k[8], kp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool on = same && j0 + u < na;
+        k[u] = on ? A.col[a0 + j0 + u] : 1;
+        kp[u] = on ? A.col[p_a0 + j0 + u] : 0;
       }
-      __syncwarp();
-      const int32_t d = __shfl_sync(kFull, k, 0) - __shfl_sync(kFull, pk, 0);
-      bool same = na <= G && pvalid && na == pna && __all_sync(kFull, lane >= na || (len == plen && k - pk == d));
-      if (same && !(d == 1 && shift1 != nullptr && __all_sync(kFull, lane >= na || shift1[k] != 0))) {
-        bool ok = true;
-        for (int j = 0; j < na && __all_sync(kFull, ok); ++j) {
-          const EntryMeta m = meta[j];
-          if (lane < m.len) ok = B.col[m.b0 + lane] - B.col[pmeta[j].b0 + lane] == d;
+      bool ok = true;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool on = same && j0 + u < na;
+        if (on) {
+          ok = ok && k[u] - kp[u] == 1 && shift1[k[u]] != 0 &&
+               B.rpt[k[u] + 1] - B.rpt[k[u]] == B.rpt[kp[u] + 1] - B.rpt[kp[u]];
         }
-        same = __all_sync(kFull, ok);
       }
-      long long n;
-      if (same) {
-        n = pn;
-        ++nreuse;
-      } else {
-        // count the row's distinct columns (the table holds any row of these bins)
+      same = same && ok;
+    }
+    const unsigned heads = __ballot_sync(kFull, valid && !same);
+    long long n = 0;
+    // heads: count distinct columns (a row without products: 0)
+    for (unsigned hm = heads; hm;) {
+      const int h = __ffs(hm) - 1;
+      hm &= hm - 1u;
+      const long long hnp = __shfl_sync(kFull, np, h);
+      long long cnt_total = 0;
+      if (hnp != 0) {
+        const int64_t ha0 = __shfl_sync(kFull, a0, h);
+        const int hna = __shfl_sync(kFull, na, h);
         const int tsz = static_cast<int>(min(static_cast<long long>(kSymReuseT),
-                                             static_cast<long long>(1) << ceil_log2_ll(2 * np)));
+                                             static_cast<long long>(1) << ceil_log2_ll(2 * hnp)));
         const int lg = max(2, 31 - __clz(tsz));
         const uint32_t hshift = 32u - static_cast<uint32_t>(lg), hmask = (1u << lg) - 1u;
         fill_empty<G>(keys, 1 << lg, lane);
+        // the head row's entries: their B rows, loaded by the lanes at once
+        int64_t hb0 = 0, hb1 = 0;
+        if (lane < hna) {
+          const int32_t k = A.col[ha0 + lane];
+          hb0 = B.rpt[k];
+          hb1 = B.rpt[k + 1];
+        }
         __syncwarp();
         int cnt = 0;
-        for (int j = 0; j < min(na, G); ++j) {
-          const EntryMeta m = meta[j];
-          for (int q = lane; q < m.len; q += G) {
-            const int32_t c = B.col[m.b0 + q];
-            uint32_t h = (static_cast<uint32_t>(c) * mult) >> hshift;
-            int32_t cur = keys[h];
+        for (int j = 0; j < hna; ++j) {
+          const int64_t q1 = __shfl_sync(kFull, hb1, j);
+          for (int64_t q = __shfl_sync(kFull, hb0, j) + lane; q < q1; q += G) {
+            const int32_t c = B.col[q];
+            uint32_t hh = (static_cast<uint32_t>(c) * mult) >> hshift;
+            int32_t cur = keys[hh];
             while (cur != c) {
               if (cur == -1) {
-                cur = atomicCAS(reinterpret_cast<int*>(keys + h), -1, c);
+                cur = atomicCAS(reinterpret_cast<int*>(keys + hh), -1, c);
                 if (cur == -1) {
                   ++cnt;
                   break;
                 }
               } else {
-                h = (h + 1) & hmask;
-                cur = *reinterpret_cast<volatile int32_t*>(keys + h);
+                hh = (hh + 1) & hmask;
+                cur = *reinterpret_cast<volatile int32_t*>(keys + hh);
               }
             }
           }
         }
-        n = static_cast<long long>(__reduce_add_sync(kFull, static_cast<unsigned>(cnt)));
-        if (na > G) n = -1;  // (host-checked: A rows <= 32) never here
+        cnt_total = static_cast<long long>(__reduce_add_sync(kFull, static_cast<unsigned>(cnt)));
+        __syncwarp();
         ++nfull;
       }
-      if (lane == 0) {
-        rpt[row] = n;
-        if (n < 0) atomicOr(&info->error, kErrTableFull);
-      }
-      pvalid = na <= G;
-      pna = na;
-      pn = n;
-      pk = k;
-      plen = len;
-      mb ^= 1;
-      __syncwarp();
+      if (lane == h) n = cnt_total;
     }
+    // copy the counts forward: a row that passed takes the last head's count
+    // before it (or, with no head before it, the previous run's last row's)
+    int src = (heads >> lane) & 1u ? lane : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, src, o);
+      if (lane >= o) src = max(src, y);
+    }
+    const long long from_head = __shfl_sync(kFull, n, max(src, 0));
+    if (src < 0) n = c_n;
+    else n = from_head;
+    if (valid) {
+      rpt[row] = n;
+      if (same) ++nreuse;
+    }
+    // carry the run's last row
+    const int last = static_cast<int>(min(static_cast<long long>(P), static_cast<long long>(rl.count - run0))) - 1;
+    c_a0 = __shfl_sync(kFull, a0, last);
+    c_na = __shfl_sync(kFull, na, last);
+    c_n = __shfl_sync(kFull, n, last);
+    cvalid = __shfl_sync(kFull, valid && np != 0, last);
   }
+  nreuse = static_cast<long long>(__reduce_add_sync(kFull, static_cast<unsigned>(nreuse)));
   if (lane == 0 && (nreuse | nfull)) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&info->reuse_rows), static_cast<unsigned long long>(nreuse));
     atomicAdd(reinterpret_cast<unsigned long long*>(&info->full_rows), static_cast<unsigned long long>(nfull));
