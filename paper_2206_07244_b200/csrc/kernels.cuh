@@ -2144,11 +2144,17 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4)
 // map for the next row. Numeric launches are made only when A's and B's
 // longest rows are <= 32 (K1); a speculative row outside that, or with more
 // than NMAX columns, is abandoned (left to the symbolic kernel).
+#ifndef SPGEMM_REUSE_U
+#define SPGEMM_REUSE_U 4      // steps' value loads in flight in the reuse path
+#endif
+#ifndef SPGEMM_REUSE_MINB
+#define SPGEMM_REUSE_MINB 5   // resident blocks per SM (48 registers)
+#endif
 constexpr int kReuseWarps = 8;
 constexpr int kReuseRows = 32;  // consecutive rows per warp (power of two)
 constexpr size_t kReuseWarpBytes = 256 * 4 + 256 + 128 * 8 + 128 * 4 + 128 * 4 + 2 * 32 * 16 + 32 * 32;  // 5376
 template <bool SPEC>
-__global__ void __launch_bounds__(32 * kReuseWarps, 5)
+__global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
     k_num_reuse(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
                 double* __restrict__ cval, uint32_t scale, DevInfo* info, Spec sp, int rows_per_warp,
                 const uint8_t* __restrict__ shift1) {
@@ -2255,7 +2261,7 @@ __global__ void __launch_bounds__(32 * kReuseWarps, 5)
         // steps' loads in flight at once, their updates in step order
         // Branch-free: a lane without a product in a step adds 0.0 into the
         // spare slot vals[NMAX] (it overlays cols[0..1], unused on this path).
-        constexpr int U = 4;
+        constexpr int U = SPGEMM_REUSE_U;
         const double* __restrict__ bval = B.val + lane;
         const uint8_t* mapl = map + lane;
         for (int j0 = 0; j0 < na; j0 += U) {
