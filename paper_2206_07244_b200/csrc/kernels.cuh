@@ -1198,6 +1198,144 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// One row of k_num_thread (lane-private TS-slot table at keys/vals, lane
+// stride 32): hash, compact, sort, write C(row,:).
+template <int TS, int NMAX>
+__device__ __forceinline__ void num_thread_row(int32_t* keys, double* vals, uint32_t mult, DevCsr A, DevCsr B,
+                                               int64_t row, int64_t base, int n, int32_t* __restrict__ ccol,
+                                               double* __restrict__ cval, DevInfo* info) {
+  auto home = [&](int32_t key) { return __umulhi(static_cast<uint32_t>(key) * mult, static_cast<uint32_t>(TS)); };
+#pragma unroll
+  for (int s = 0; s < TS; ++s) {
+    keys[s * 32] = -1;
+    vals[s * 32] = 0.0;
+  }
+  const int64_t a1 = A.rpt[row + 1];
+  // A entries two at a time: both B row ranges, then up to QB entries of each
+  // B row, are loaded before any is inserted (independent loads in flight
+  // instead of one dependent chain per product)
+  constexpr int QB = 8;
+  for (int64_t p = A.rpt[row]; p < a1; p += 2) {
+    const bool two = p + 1 < a1;
+    const int32_t k0 = A.col[p];
+    const int32_t k1 = two ? A.col[p + 1] : k0;
+    const double av0 = A.val[p];
+    const double av1 = two ? A.val[p + 1] : 0.0;
+    const int64_t q0 = B.rpt[k0], e0 = B.rpt[k0 + 1];
+    const int64_t q1 = B.rpt[k1], e1 = two ? B.rpt[k1 + 1] : q1;
+    auto insert = [&](int32_t key, double x) {
+      uint32_t h = home(key);
+      while (true) {
+        const int32_t c = keys[h * 32];
+        if (c == key) break;
+        if (c == -1) {
+          keys[h * 32] = key;
+          break;
+        }
+        h = h + 1 == TS ? 0u : h + 1;
+      }
+      vals[h * 32] = __dadd_rn(vals[h * 32], x);
+    };
+    int32_t c0[QB], c1[QB];
+    double v0[QB], v1[QB];
+#pragma unroll
+    for (int i = 0; i < QB; ++i) {
+      c0[i] = q0 + i < e0 ? B.col[q0 + i] : -1;
+      v0[i] = q0 + i < e0 ? B.val[q0 + i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < QB; ++i) {
+      c1[i] = q1 + i < e1 ? B.col[q1 + i] : -1;
+      v1[i] = q1 + i < e1 ? B.val[q1 + i] : 0.0;
+    }
+    // entry p (its whole B row) strictly before entry p + 1: the reference's order
+#pragma unroll
+    for (int i = 0; i < QB; ++i)
+      if (c0[i] >= 0) insert(c0[i], __dmul_rn(av0, v0[i]));
+    for (int64_t q = q0 + QB; q < e0; ++q) insert(B.col[q], __dmul_rn(av0, B.val[q]));
+#pragma unroll
+    for (int i = 0; i < QB; ++i)
+      if (c1[i] >= 0) insert(c1[i], __dmul_rn(av1, v1[i]));
+    for (int64_t q = q1 + QB; q < e1; ++q) insert(B.col[q], __dmul_rn(av1, B.val[q]));
+  }
+  // compact in place: entry m <- slot s (m <= s), keys and values together
+  int m = 0;
+  int32_t kmin = 0x7fffffff, kmax = -1;
+#pragma unroll
+  for (int s = 0; s < TS; ++s) {
+    const int32_t c = keys[s * 32];
+    if (c != -1) {
+      keys[m * 32] = c;
+      vals[m * 32] = vals[s * 32];
+      kmin = min(kmin, c);
+      kmax = max(kmax, c);
+      ++m;
+    }
+  }
+  if (m != n) atomicOr(&info->error, kErrNumericCount);
+  constexpr int LG = log2_const<NMAX>();
+  if (static_cast<uint32_t>(kmax - kmin) < (0xffffffffu >> LG)) {
+    // narrow row: 32-bit keys (col - kmin) << LG | entry, sorted with min/max pairs
+    uint32_t v[NMAX];
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i)
+      v[i] = i < m ? (static_cast<uint32_t>(keys[i * 32] - kmin) << LG) | static_cast<uint32_t>(i) : 0xffffffffu;
+#pragma unroll
+    for (int k = 2; k <= NMAX; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+        for (int i = 0; i < NMAX; ++i) {
+          const int pi = i ^ j;
+          if (pi > i) {
+            const uint32_t a = v[i], b = v[pi];
+            const bool up = (i & k) == 0;
+            v[i] = up ? min(a, b) : max(a, b);
+            v[pi] = up ? max(a, b) : min(a, b);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      if (i < m) {
+        ccol[base + i] = kmin + static_cast<int32_t>(v[i] >> LG);
+        cval[base + i] = vals[(v[i] & (NMAX - 1u)) * 32];
+      }
+    }
+    return;
+  }
+  unsigned long long v[NMAX];
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i)
+    v[i] = i < m ? (static_cast<unsigned long long>(static_cast<uint32_t>(keys[i * 32])) << 32) | static_cast<uint32_t>(i)
+                 : ~0ull;
+#pragma unroll
+  for (int k = 2; k <= NMAX; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NMAX; ++i) {
+        const int pi = i ^ j;
+        if (pi > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = v[i], b = v[pi];
+          const bool sw = up ? (a > b) : (a < b);
+          v[i] = sw ? b : a;
+          v[pi] = sw ? a : b;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) {
+    if (i < m) {
+      ccol[base + i] = static_cast<int32_t>(v[i] >> 32);
+      cval[base + i] = vals[static_cast<uint32_t>(v[i]) * 32];
+    }
+  }
+}
+
 // Thread-per-row numeric kernel for rows with nnz <= NMAX (TS >= 1.5*NMAX slots,
 // any TS: the home slot is the high product of the Fibonacci hash and TS, so a
 // 24-slot table (288 B/thread instead of 384) fits 6 blocks per SM instead of 4):
@@ -1216,7 +1354,6 @@ __global__ void __launch_bounds__(128)
   int32_t* keys = reinterpret_cast<int32_t*>(smem_raw + static_cast<size_t>(blockDim.x) * TS * 8) +
                   warp * TS * 32 + lane;
   const Hash hs = make_hash(scale, 5);  // its multiplier; the slot range is TS
-  auto home = [&](int32_t key) { return __umulhi(static_cast<uint32_t>(key) * hs.mult, static_cast<uint32_t>(TS)); };
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rl.count; idx += stride) {
     const int64_t row = rl.row(idx);
@@ -1224,135 +1361,7 @@ __global__ void __launch_bounds__(128)
     const int n = static_cast<int>(rpt[row + 1] - base);
     if (n == 0) continue;
     if (sp.done(row)) continue;  // computed in the symbolic phase, copied by k_spec_copy
-#pragma unroll
-    for (int s = 0; s < TS; ++s) {
-      keys[s * 32] = -1;
-      vals[s * 32] = 0.0;
-    }
-    const int64_t a1 = A.rpt[row + 1];
-    // A entries two at a time: both B row ranges, then up to QB entries of each
-    // B row, are loaded before any is inserted (independent loads in flight
-    // instead of one dependent chain per product)
-    constexpr int QB = 8;
-    for (int64_t p = A.rpt[row]; p < a1; p += 2) {
-      const bool two = p + 1 < a1;
-      const int32_t k0 = A.col[p];
-      const int32_t k1 = two ? A.col[p + 1] : k0;
-      const double av0 = A.val[p];
-      const double av1 = two ? A.val[p + 1] : 0.0;
-      const int64_t q0 = B.rpt[k0], e0 = B.rpt[k0 + 1];
-      const int64_t q1 = B.rpt[k1], e1 = two ? B.rpt[k1 + 1] : q1;
-      auto insert = [&](int32_t key, double x) {
-        uint32_t h = home(key);
-        while (true) {
-          const int32_t c = keys[h * 32];
-          if (c == key) break;
-          if (c == -1) {
-            keys[h * 32] = key;
-            break;
-          }
-          h = h + 1 == TS ? 0u : h + 1;
-        }
-        vals[h * 32] = __dadd_rn(vals[h * 32], x);
-      };
-      int32_t c0[QB], c1[QB];
-      double v0[QB], v1[QB];
-#pragma unroll
-      for (int i = 0; i < QB; ++i) {
-        c0[i] = q0 + i < e0 ? B.col[q0 + i] : -1;
-        v0[i] = q0 + i < e0 ? B.val[q0 + i] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < QB; ++i) {
-        c1[i] = q1 + i < e1 ? B.col[q1 + i] : -1;
-        v1[i] = q1 + i < e1 ? B.val[q1 + i] : 0.0;
-      }
-      // entry p (its whole B row) strictly before entry p + 1: the reference's order
-#pragma unroll
-      for (int i = 0; i < QB; ++i)
-        if (c0[i] >= 0) insert(c0[i], __dmul_rn(av0, v0[i]));
-      for (int64_t q = q0 + QB; q < e0; ++q) insert(B.col[q], __dmul_rn(av0, B.val[q]));
-#pragma unroll
-      for (int i = 0; i < QB; ++i)
-        if (c1[i] >= 0) insert(c1[i], __dmul_rn(av1, v1[i]));
-      for (int64_t q = q1 + QB; q < e1; ++q) insert(B.col[q], __dmul_rn(av1, B.val[q]));
-    }
-    // compact in place: entry m <- slot s (m <= s), keys and values together
-    int m = 0;
-    int32_t kmin = 0x7fffffff, kmax = -1;
-#pragma unroll
-    for (int s = 0; s < TS; ++s) {
-      const int32_t c = keys[s * 32];
-      if (c != -1) {
-        keys[m * 32] = c;
-        vals[m * 32] = vals[s * 32];
-        kmin = min(kmin, c);
-        kmax = max(kmax, c);
-        ++m;
-      }
-    }
-    if (m != n) atomicOr(&info->error, kErrNumericCount);
-    constexpr int LG = log2_const<NMAX>();
-    if (static_cast<uint32_t>(kmax - kmin) < (0xffffffffu >> LG)) {
-      // narrow row: 32-bit keys (col - kmin) << LG | entry, sorted with min/max pairs
-      uint32_t v[NMAX];
-#pragma unroll
-      for (int i = 0; i < NMAX; ++i)
-        v[i] = i < m ? (static_cast<uint32_t>(keys[i * 32] - kmin) << LG) | static_cast<uint32_t>(i) : 0xffffffffu;
-#pragma unroll
-      for (int k = 2; k <= NMAX; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-          for (int i = 0; i < NMAX; ++i) {
-            const int pi = i ^ j;
-            if (pi > i) {
-              const uint32_t a = v[i], b = v[pi];
-              const bool up = (i & k) == 0;
-              v[i] = up ? min(a, b) : max(a, b);
-              v[pi] = up ? max(a, b) : min(a, b);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < NMAX; ++i) {
-        if (i < m) {
-          ccol[base + i] = kmin + static_cast<int32_t>(v[i] >> LG);
-          cval[base + i] = vals[(v[i] & (NMAX - 1u)) * 32];
-        }
-      }
-      continue;
-    }
-    unsigned long long v[NMAX];
-#pragma unroll
-    for (int i = 0; i < NMAX; ++i)
-      v[i] = i < m ? (static_cast<unsigned long long>(static_cast<uint32_t>(keys[i * 32])) << 32) | static_cast<uint32_t>(i)
-                   : ~0ull;
-#pragma unroll
-    for (int k = 2; k <= NMAX; k <<= 1) {
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-        for (int i = 0; i < NMAX; ++i) {
-          const int pi = i ^ j;
-          if (pi > i) {
-            const bool up = (i & k) == 0;
-            const unsigned long long a = v[i], b = v[pi];
-            const bool sw = up ? (a > b) : (a < b);
-            v[i] = sw ? b : a;
-            v[pi] = sw ? a : b;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
-      if (i < m) {
-        ccol[base + i] = static_cast<int32_t>(v[i] >> 32);
-        cval[base + i] = vals[static_cast<uint32_t>(v[i]) * 32];
-      }
-    }
+    num_thread_row<TS, NMAX>(keys, vals, hs.mult, A, B, row, base, n, ccol, cval, info);
   }
 }
 
