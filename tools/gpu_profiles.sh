@@ -16,6 +16,8 @@ for c in 2 1 4 3; do
 done
 timeout 900 python bench.py --config 5 --rmat-scale 22 --steps 3 --warmup 3 > gpurun_out/${R}_bench_c5_s22.log 2>&1
 tail -1 gpurun_out/${R}_bench_c5_s22.log > gpurun_out/${R}_bench_c5_s22.json
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${R}_bench_reference_c2.log 2>&1
+tail -1 gpurun_out/${R}_bench_reference_c2.log > gpurun_out/${R}_bench_reference_c2.json
 fi
 for c in 2 1 4; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
