@@ -29,6 +29,7 @@
 #include "kernels.cuh"
 #include "kernels_heap.cuh"
 #include "kernels_coo.cuh"
+#include "kernels_reuse.cuh"
 #include "spgemm_capi.h"
 
 using namespace spgemm_b200;
@@ -270,11 +271,11 @@ int persistent_grid(spgemm_ctx* ctx, Kern kern, int threads, size_t smem, int64_
 // predecessor; a small bin needs short runs to spread over the SMs).
 // SPGEMM_REUSE_ROWS overrides (experiments).
 template <typename Kern>
-int reuse_rows_per_warp(spgemm_ctx* ctx, Kern kern, size_t smem, int64_t rows) {
+int reuse_rows_per_warp(spgemm_ctx* ctx, Kern kern, size_t smem, int64_t rows, int block_warps = kReuseWarps) {
   if (const char* e = std::getenv("SPGEMM_REUSE_ROWS")) return std::max(1, std::min(kReuseRows, std::atoi(e)));
   int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kReuseWarps, smem), "occupancy");
-  const int64_t warps = static_cast<int64_t>(std::max(per_sm, 1)) * ctx->num_sms * kReuseWarps;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * block_warps, smem), "occupancy");
+  const int64_t warps = static_cast<int64_t>(std::max(per_sm, 1)) * ctx->num_sms * block_warps;
   int r = kReuseRows;
   while (r > 1 && rows < warps * r) r >>= 1;
   return r;
@@ -487,7 +488,8 @@ struct spgemm_pipeline {
   bool heap_ordered() const { return opts.ordered_heap || opts.deterministic; }
   bool heap_bitmap() const { return idx32; }  // bitmap kernels (ordered or atomic); else k_num_global
   int32_t* d_poff = nullptr;                   // ordered bitmap tier: B's column-panel offsets
-  uint8_t* d_shift1 = nullptr;                 // k_num_reuse: B row k == B row k-1 shifted by one (arena)
+  uint8_t* d_shift1 = nullptr;                 // B row k == B row k-1 shifted by one (arena)
+  uint8_t* d_rflag = nullptr;                  // row i's structure == row i-1's shifted by one (arena)
 };
 
 namespace {
@@ -598,6 +600,8 @@ void spgemm_pipeline::setup() {
   const bool use_shift = reuse_route;
   const size_t o_shift = off;
   if (use_shift) off = align_up(o_shift + static_cast<size_t>(std::max<int64_t>(b_rows, 1)), 256);
+  const size_t o_rflag = off;
+  if (use_shift) off = align_up(o_rflag + static_cast<size_t>(std::max<int64_t>(M, 1)), 256);
   arena_bytes = off;
   d_arena = static_cast<unsigned char*>(scratch_acquire(ctx, arena_bytes, s));
   metadata_calls += 1;
@@ -607,10 +611,15 @@ void spgemm_pipeline::setup() {
   d_bins = reinterpret_cast<int64_t*>(d_arena + o_bins);
   d_spill = reinterpret_cast<int64_t*>(d_arena + o_spill);
   d_shift1 = nullptr;
+  d_rflag = nullptr;
   if (use_shift && b_rows > 0) {
     d_shift1 = d_arena + o_shift;
     const int fg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(b_rows, 256)));
     SPG_LAUNCH(ctx, "k_shift_flags", s, k_shift_flags<<<std::max(fg, 1), 256, 0, s>>>(B, d_shift1));
+    d_rflag = d_arena + o_rflag;
+    const int a_is_b = A.rpt == B.rpt && A.col == B.col;
+    const int rg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(M, 256)));
+    SPG_LAUNCH(ctx, "k_reuse_flags", s, k_reuse_flags<<<std::max(rg, 1), 256, 0, s>>>(A, d_shift1, d_rflag, a_is_b));
   }
   if (use_spec) {
     spec = Spec{reinterpret_cast<int32_t*>(d_arena + o_scol), reinterpret_cast<double*>(d_arena + o_sval),
@@ -671,7 +680,7 @@ void spgemm_pipeline::launch_sym_bin(int bin, const RowList& rl, cudaStream_t s)
     // (the bin's size is on the device: the kernel sizes its runs from it)
     const int grid = persistent_grid(ctx, k_sym_reuse, 32 * kSymReuseWarps, smem, ceil_div(rl.count, kSymReuseWarps));
     SPG_LAUNCH(ctx, "k_sym_reuse", s,
-               k_sym_reuse<<<grid, 32 * kSymReuseWarps, smem, s>>>(rl, A, B, d_rpt, scale, 0, d_shift1, d_info_sym));
+               k_sym_reuse<<<grid, 32 * kSymReuseWarps, smem, s>>>(rl, A, B, d_rpt, scale, 0, d_rflag, d_info_sym));
     return;
   }
   auto group = [&](auto kern, int G, int T, int NGRP, int WB) {
@@ -934,14 +943,14 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
       // row): structure reuse; other products (the RAP chain's A*P, R*AP):
       // the dense-index kernel
       if (reuse_route) {
-        auto kern = &k_num_reuse<false>;
-        const size_t smem = static_cast<size_t>(kReuseWarps) * kReuseWarpBytes;
+        auto kern = &k_num_reuse_multi;
+        const size_t smem = static_cast<size_t>(kMultiWarps) * kMultiWarpBytes;
         prepare_kernel(ctx, kern, smem);
-        const int rpw = reuse_rows_per_warp(ctx, kern, smem, rl.count);
-        const int grid = persistent_grid(ctx, kern, 32 * kReuseWarps, smem, ceil_div(rl.count, kReuseWarps * rpw));
-        SPG_LAUNCH(ctx, "k_num_reuse", s,
-                   kern<<<grid, 32 * kReuseWarps, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec,
-                                                            rpw, d_shift1));
+        const int rpw = reuse_rows_per_warp(ctx, kern, smem, rl.count, kMultiWarps);
+        const int grid = persistent_grid(ctx, kern, 32 * kMultiWarps, smem, ceil_div(rl.count, kMultiWarps * rpw));
+        SPG_LAUNCH(ctx, "k_num_reuse_multi", s,
+                   kern<<<grid, 32 * kMultiWarps, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec,
+                                                            rpw, d_rflag));
       } else {
         auto kern = &k_num_lean<false>;
         const size_t smem = static_cast<size_t>(kLeanGroups) * kLeanGroupBytes;

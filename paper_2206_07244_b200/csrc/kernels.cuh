@@ -791,6 +791,25 @@ __device__ __forceinline__ int group_max(int v, unsigned gm) {
 // per-column summation order.
 // Per-entry metadata of one A-row chunk, staged in shared memory so each step
 // reads it with one broadcast 16-byte load.
+// shared-window f64 load/store by 32-bit address; volatile: kept in program order
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
+}
+// predicated read-only global f64 load (0.0 when !on)
+__device__ __forceinline__ double ldg_f64_if(const void* p, bool on) {
+  double v = 0.0;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.f64 %0, [%1];\n\t}"
+      : "+d"(v)
+      : "l"(p), "r"(static_cast<int>(on)));
+  return v;
+}
+
 struct EntryMeta {
   int32_t b0;   // B row start (32-bit index path)
   int32_t len;  // B row length
@@ -2157,11 +2176,13 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4)
 #define SPGEMM_REUSE_U 4      // steps' value loads in flight in the reuse path
 #endif
 #ifndef SPGEMM_REUSE_MINB
-#define SPGEMM_REUSE_MINB 5   // resident blocks per SM (48 registers)
+#define SPGEMM_REUSE_MINB 4   // resident blocks per SM (64 registers)
 #endif
 constexpr int kReuseWarps = 8;
 constexpr int kReuseRows = 32;  // consecutive rows per warp (power of two)
-constexpr size_t kReuseWarpBytes = 256 * 4 + 256 + 128 * 8 + 128 * 4 + 128 * 4 + 2 * 32 * 16 + 32 * 32;  // 5376
+constexpr size_t kReuseWarpBytes = 256 * 4 + 256 + 128 * 8 + 128 * 4 + 128 * 4 + 2 * 32 * 16 + 32 * 32 * 2;  // 6400
+// the map holds 16-bit shared-window addresses: the block's window must stay below 64 KB
+static_assert(kReuseWarps * kReuseWarpBytes + 1024 < 65536, "k_num_reuse map addresses are 16-bit");
 template <bool SPEC>
 __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
     k_num_reuse(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, int32_t* __restrict__ ccol,
@@ -2180,7 +2201,10 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
   int32_t* cols = reinterpret_cast<int32_t*>(wb + T * 5 + NMAX * 8);      // [NMAX] claim order
   int32_t* ocols = reinterpret_cast<int32_t*>(wb + T * 5 + NMAX * 12);    // [NMAX] previous row's output
   EntryMeta* metab = reinterpret_cast<EntryMeta*>(wb + T * 5 + NMAX * 16);  // [2][32]
-  uint8_t* map = wb + T * 5 + NMAX * 16 + 2 * 32 * 16;                   // [32][32] product -> position
+  // [32][32] product -> the shared address of its output's accumulator (during
+  // the full path's walk: the product's dense index)
+  uint16_t* map = reinterpret_cast<uint16_t*>(wb + T * 5 + NMAX * 16 + 2 * 32 * 16);
+  const uint32_t vals_sa = static_cast<uint32_t>(__cvta_generic_to_shared(vals));
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t mult = scale * 0x9E3779B1u;
   // previous row (warp-uniform except the per-lane entry fields)
@@ -2199,7 +2223,7 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
   }
   const int64_t first = (static_cast<int64_t>(blockIdx.x) * kReuseWarps + warp) * R;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kReuseWarps * R;
-  long long nreuse = 0, nfull = 0;  // rows through each path (DevInfo counters)
+  unsigned nreuse = 0, nfull = 0;  // rows through each path (DevInfo counters)
   for (int64_t run0 = first; run0 < rl.count; run0 += stride) {
    // the run's row ids and skip tests, 32 at a time; then its rows in order
    // the run's row ids, skip tests, C offsets / nprod and A-row bounds, one row per lane
@@ -2249,8 +2273,8 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
       const int64_t r0 = B.rpt[k];
       len = static_cast<int>(B.rpt[k + 1] - r0);
       b0 = static_cast<int32_t>(r0);
-      meta[lane] = EntryMeta{b0, len, av};
     }
+    meta[lane] = EntryMeta{b0, len, av};  // rows j >= na: len 0 (the reuse loop's padding)
     const int maxlen = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(len)));
     if (na > G || maxlen > G) {  // (speculative rows only) left to the symbolic + generic kernels
       pvalid = false;
@@ -2271,31 +2295,39 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
         // Branch-free: a lane without a product in a step adds 0.0 into the
         // spare slot vals[NMAX] (it overlays cols[0..1], unused on this path).
         constexpr int U = SPGEMM_REUSE_U;
-        const double* __restrict__ bval = B.val + lane;
-        const uint8_t* mapl = map + lane;
+        static_assert(G % U == 0, "U must divide the warp width (meta/map rows >= na are padding)");
+        // per-lane base pointer: a step's address is one 32x32->64 multiply-add
+        const char* bvl = reinterpret_cast<const char*>(B.val + lane);
+        const uint16_t* mapl = map + lane;
+        // accumulators start at +0.0 (the reference's fold starts from 0.0)
+        for (int e = lane; e < pn; e += G) vals[e] = 0.0;
+        __syncwarp();
+#pragma unroll 1
         for (int j0 = 0; j0 < na; j0 += U) {
+          const EntryMeta* mj = meta + j0;
+          const uint16_t* mp = mapl + j0 * G;
           double bv[U], av[U];
-          int pos[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int j = j0 + u;
-            const EntryMeta m = meta[(j0 + u) & (G - 1)];
-            const bool on = j < na && lane < m.len;
+            // rows j >= na: len 0 (their map rows are all spare)
+            const EntryMeta m = mj[u];
             av[u] = m.av;
-            bv[u] = on ? bval[m.b0] : 0.0;
-            // low 7 bits: the position (NMAX: the spare slot); bit 8: first product
-            const int pm = on ? mapl[j * G] : 0x80;
-            pos[u] = on ? (pm & 0x7f) | ((pm & 0x80) << 1) : NMAX | 0x100;
+            bv[u] = ldg_f64_if(bvl + static_cast<size_t>(static_cast<uint32_t>(m.b0)) * 8u, lane < m.len);
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int pu = pos[u] & 0xff;
-            const double prev = (pos[u] & 0x100) ? 0.0 : vals[pu];
-            vals[pu] = __dadd_rn(prev, __dmul_rn(av[u], bv[u]));
-            __syncwarp();
+            // a lane without a product (lane >= len, or j >= na) maps to the
+            // spare slot vals[NMAX] (it overlays cols[0..1], unused here); the
+            // volatile shared accesses keep the steps in order (the warp is
+            // converged: no branch inside the loop)
+            const uint32_t a = mp[u * G];
+            sts_f64(a, __dadd_rn(lds_f64(a), __dmul_rn(av[u], bv[u])));
           }
         }
+        __syncwarp();
       } else {
+        for (int e = lane; e < pn; e += G) vals[e] = 0.0;
+        __syncwarp();
         for (int j = 0; j < na; ++j) {
           const EntryMeta m = meta[j];
           if (lane < m.len) {
@@ -2303,10 +2335,10 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
             const int32_t cp = B.col[pmeta[j].b0 + lane];
             const double x = __dmul_rn(m.av, B.val[m.b0 + lane]);
             ok = ok && c - cp == d;
-            const int pm = map[j * G + lane];
-            const int pos = pm & 0x7f;
-            vals[pos] = __dadd_rn((pm & 0x80) ? 0.0 : vals[pos], x);
+            const uint32_t a = map[j * G + lane];
+            sts_f64(a, __dadd_rn(lds_f64(a), x));
           }
+          __syncwarp();
           if (!__all_sync(kFull, ok)) break;  // structure differs: stop early (the full path recomputes)
         }
       }
@@ -2376,7 +2408,7 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
         const int ix = fresh ? nk + __popc(cb & lt) : sidx[h];
         const double prev = fresh ? 0.0 : vals[ix];
         vals[ix] = __dadd_rn(prev, x);
-        map[j * G + lane] = static_cast<uint8_t>(ix);
+        map[j * G + lane] = static_cast<uint16_t>(ix);
         if (fresh) {
           sidx[h] = static_cast<uint8_t>(ix);
           cols[ix] = c;
@@ -2427,21 +2459,13 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
       rank[ix] = static_cast<uint8_t>(e);
     }
     __syncwarp();
-    // product -> output position for the next row, bit 7 set on the first
-    // product (in A order) of its position: the reuse path writes 0.0 + x
-    // there instead of reading a zeroed accumulator
-    uint8_t* seen = reinterpret_cast<uint8_t*>(cols);  // (the claim-order columns are consumed)
-    for (int e = lane; e < NMAX; e += G) seen[e] = 0;
-    __syncwarp();
-    for (int j = 0; j < na; ++j) {
-      if (lane < __shfl_sync(kFull, len, j)) {
-        const int p = rank[map[j * G + lane]];
-        const int first = seen[p] == 0 ? 0x80 : 0;
-        seen[p] = 1;
-        map[j * G + lane] = static_cast<uint8_t>(p | first);
-      }
-      __syncwarp();
+    // product -> output position for the next row; map rows j >= na and lanes
+    // past a B row's length point at the spare slot NMAX
+    for (int j = 0; j < G; ++j) {
+      const int lj = __shfl_sync(kFull, len, j);
+      map[j * G + lane] = static_cast<uint16_t>(vals_sa + 8u * ((j < na && lane < lj) ? rank[map[j * G + lane]] : NMAX));
     }
+    __syncwarp();
     if constexpr (SPEC) {
       if (lane == 0) {
         rpt[row] = n;
@@ -2465,28 +2489,23 @@ __global__ void __launch_bounds__(32 * kReuseWarps, SPGEMM_REUSE_MINB)
 }
 
 // Symbolic phase of the structure-reuse route (A*A-shaped products with
-// warp-sized A and B rows, e.g. 3-D stencils): nnz(C(i,:)) = nnz(C(i',:)) of
-// the warp's previous row i' whenever row i's structure is row i''s shifted
-// by d (the exact test of k_num_reuse: A-row lengths, entry-wise B-row lengths
-// and k_j(i) - k_j(i') = d; then either the per-B-row shift flags (d = 1) or a
-// per-product column check). Only rows that fail the test count their distinct
+// warp-sized A and B rows, e.g. 3-D stencils): nnz(C(i,:)) = nnz(C(i-1,:))
+// whenever row i is flagged by k_reuse_flags (its structure is row i-1's
+// shifted by one: kernels_reuse.cuh). Only unflagged rows count their distinct
 // columns, with a 1024-slot table (a symbolic bin of <= 1024 products cannot
-// fill it). No values, no sort: the numeric phase (k_num_reuse) then writes C
-// in place -- no speculative scratch, no copy.
+// fill it). No values, no sort: the numeric phase (k_num_reuse_multi) then
+// writes C in place -- no speculative scratch, no copy.
 constexpr int kSymReuseWarps = 8;
 constexpr int kSymReuseT = 1024;
 constexpr size_t kSymReuseWarpBytes = kSymReuseT * 4 + 2 * 32 * 16;
 __global__ void __launch_bounds__(32 * kSymReuseWarps)
     k_sym_reuse(RowList rl_in, DevCsr A, DevCsr B, int64_t* __restrict__ rpt, uint32_t scale, int rows_per_warp,
-                const uint8_t* __restrict__ shift1, DevInfo* info) {
-  // A warp takes runs of 32 consecutive rows of the bin, one row per lane:
-  // every lane tests ITS row against the row before it in the bin (lane - 1;
-  // lane 0: the previous run's last row) -- all 32 tests at once, the loads of
-  // different rows independent. Exact test for d = 1: equal A-row length,
-  // k_j(i) - k_j(i-1) = 1 and equal B-row lengths for every entry, and the
-  // per-B-row shift flag of every k_j(i). A row that passes has its
-  // predecessor's count; the others ("heads") count their distinct columns,
-  // warp-cooperatively, and the counts are copied forward lane to lane.
+                const uint8_t* __restrict__ rflag, DevInfo* info) {
+  // A warp takes runs of 32 consecutive rows of the bin, one row per lane: a
+  // flagged row whose predecessor in the bin (lane - 1; lane 0: the previous
+  // piece's last row) is row - 1 has that row's count; the others ("heads")
+  // count their distinct columns, warp-cooperatively, and the counts are
+  // copied forward lane to lane.
   constexpr int G = 32;
   const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2505,8 +2524,7 @@ __global__ void __launch_bounds__(32 * kSymReuseWarps)
     while (R > 4 && rl.count < warps * R) R >>= 1;
   }
   bool cvalid = false;  // the previous piece's last row (warp-uniform)
-  int64_t c_a0 = 0;
-  int c_na = 0;
+  int64_t c_row = -2;
   long long c_n = 0;
   long long nreuse = 0, nfull = 0;
   const int64_t first = (static_cast<int64_t>(blockIdx.x) * kSymReuseWarps + warp) * R;
@@ -2515,45 +2533,26 @@ __global__ void __launch_bounds__(32 * kSymReuseWarps)
   for (int64_t run0 = first; run0 < rl.count; run0 += (run0 - first) % R + P >= R ? stride - (R - P) : P) {
     if ((run0 - first) % R == 0) cvalid = false;  // a new run: its first row is a head
     const bool valid = lane < P && run0 + lane < rl.count;
-    int64_t row = 0, a0 = 0;
+    int64_t row = -1, a0 = 0;
     long long np = 0;
     int na = 0;
+    bool fl = false;
     if (valid) {
       row = rl.row(run0 + lane);
       np = rpt[row];
       a0 = A.rpt[row];
       na = static_cast<int>(A.rpt[row + 1] - a0);
+      fl = rflag[row] != 0;
     }
-    // the predecessor in the bin: lane - 1, or the previous run's last row
-    int64_t p_a0 = __shfl_up_sync(kFull, a0, 1);
-    int p_na = __shfl_up_sync(kFull, na, 1);
+    // the predecessor in the bin: lane - 1, or the previous run's last row; a
+    // flagged row whose predecessor is row - 1 has its count
+    int64_t p_row = __shfl_up_sync(kFull, row, 1);
     bool p_ok = __shfl_up_sync(kFull, valid && np != 0, 1);
     if (lane == 0) {
-      p_a0 = c_a0;
-      p_na = c_na;
+      p_row = c_row;
       p_ok = cvalid;
     }
-    bool same = valid && np != 0 && p_ok && na == p_na && na <= G && shift1 != nullptr;
-    // 8 entries per round, all their loads issued before any is tested
-    for (int j0 = 0; __any_sync(kFull, same && j0 < na); j0 += 8) {
-      int32_t k[8], kp[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool on = same && j0 + u < na;
-        k[u] = on ? A.col[a0 + j0 + u] : 1;
-        kp[u] = on ? A.col[p_a0 + j0 + u] : 0;
-      }
-      bool ok = true;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool on = same && j0 + u < na;
-        if (on) {
-          ok = ok && k[u] - kp[u] == 1 && shift1[k[u]] != 0 &&
-               B.rpt[k[u] + 1] - B.rpt[k[u]] == B.rpt[kp[u] + 1] - B.rpt[kp[u]];
-        }
-      }
-      same = same && ok;
-    }
+    const bool same = valid && np != 0 && p_ok && fl && p_row + 1 == row;
     const unsigned heads = __ballot_sync(kFull, valid && !same);
     long long n = 0;
     // heads: count distinct columns (a row without products: 0)
@@ -2622,8 +2621,7 @@ __global__ void __launch_bounds__(32 * kSymReuseWarps)
     }
     // carry the run's last row
     const int last = static_cast<int>(min(static_cast<long long>(P), static_cast<long long>(rl.count - run0))) - 1;
-    c_a0 = __shfl_sync(kFull, a0, last);
-    c_na = __shfl_sync(kFull, na, last);
+    c_row = __shfl_sync(kFull, row, last);
     c_n = __shfl_sync(kFull, n, last);
     cvalid = __shfl_sync(kFull, valid && np != 0, last);
   }

@@ -79,20 +79,20 @@ def test_short_rows_signed_zeros(sg, oracle):
 @pytest.mark.parametrize("n", [5, 9, 17, 40])
 def test_wide_route_stencils(sg, oracle, n):
     a = S.random_values(S.stencil3d_27pt(n), n)
-    _run(sg, oracle, a, a, "k_num_reuse")
+    _run(sg, oracle, a, a, "k_num_reuse_multi")
 
 
 @pytest.mark.parametrize("frac,seed", [(0.001, 4), (0.05, 5)])
 def test_wide_route_broken_chains(sg, oracle, frac, seed):
     a = S.random_values(_drop(S.stencil3d_27pt(30), frac, seed), seed)
-    _run(sg, oracle, a, a, "k_num_reuse")
+    _run(sg, oracle, a, a, "k_num_reuse_multi")
 
 
 def test_wide_route_signed_zeros(sg, oracle):
     a = S.stencil3d_27pt(12)
     rng = np.random.default_rng(6)
     v = rng.choice(np.array([-0.0, 0.0, 1.0, -1.0, 0.5]), size=a.val.size)
-    _run(sg, oracle, CsrMatrix(a.rows, a.cols, a.rpt, a.col, v), CsrMatrix(a.rows, a.cols, a.rpt, a.col, v), "k_num_reuse")
+    _run(sg, oracle, CsrMatrix(a.rows, a.cols, a.rpt, a.col, v), CsrMatrix(a.rows, a.cols, a.rpt, a.col, v), "k_num_reuse_multi")
 
 
 def test_routes_off_matches(sg, oracle, monkeypatch):
@@ -103,3 +103,32 @@ def test_routes_off_matches(sg, oracle, monkeypatch):
     without = sg.multiply(a, a).c.to_host()
     assert np.array_equal(with_reuse.col, without.col)
     assert np.array_equal(with_reuse.val.view(np.int64), without.val.view(np.int64))
+
+
+@pytest.mark.parametrize("n", [16, 48])
+def test_wide_route_distinct_operands(sg, oracle, n):
+    # A and B of one pattern in separate arrays: the row flags compare A's rows
+    # themselves instead of reading B's shift flags for them
+    a = S.random_values(S.stencil3d_27pt(n), 21)
+    b = S.random_values(S.stencil3d_27pt(n), 22)
+    b = CsrMatrix(b.rows, b.cols, b.rpt.copy(), b.col.copy(), b.val)
+    _run(sg, oracle, a, b, "k_num_reuse_multi")
+
+
+@pytest.mark.parametrize("frac,seed", [(0.002, 7), (0.05, 8)])
+def test_wide_route_other_b_pattern(sg, oracle, frac, seed):
+    # B's pattern differs from A's (dropped entries): A's row shifts hold, B's
+    # shift flags break the chains wherever a dropped entry is referenced
+    a = S.random_values(S.stencil3d_27pt(20), seed)
+    b = S.random_values(_drop(S.stencil3d_27pt(20), frac, seed + 100), seed + 1)
+    b = CsrMatrix(b.rows, b.cols, b.rpt, b.col, b.val)
+    out = sg.multiply(a, b)
+    assert_matches_oracle(out.c, oracle.spgemm(a, b))
+
+
+def test_wide_route_repeatable(sg, oracle):
+    a = S.random_values(S.stencil3d_27pt(40), 31)
+    first = sg.multiply(a, a).c.to_host()
+    again = sg.multiply(a, a).c.to_host()
+    assert np.array_equal(first.col, again.col)
+    assert np.array_equal(first.val.view(np.int64), again.val.view(np.int64))

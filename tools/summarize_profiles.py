@@ -30,7 +30,7 @@ def short_name(full):
             keep = keep[:2]
             if name == "k_num_group" and last in ("1", "true"):
                 keep.append("spec")  # the speculative instance of the symbolic phase
-        elif name in ("k_num_lean", "k_num_reuse", "k_num_pair"):
+        elif name in ("k_num_lean", "k_num_reuse", "k_num_reuse_multi", "k_num_pair"):
             keep = ["spec"] if last in ("1", "true") else []
         elif name in ("k_sym_block", "k_num_block"):
             keep = keep[:1]
