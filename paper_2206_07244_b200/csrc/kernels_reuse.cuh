@@ -68,7 +68,10 @@ __global__ void __launch_bounds__(256)
 #endif
 constexpr int kMultiWarps = 4;
 constexpr int kMultiM = 4;               // flagged rows folded together
-constexpr int kMultiU = 4;               // steps whose B values are loaded together
+#ifndef SPGEMM_MULTI_U
+#define SPGEMM_MULTI_U 2
+#endif
+constexpr int kMultiU = SPGEMM_MULTI_U;  // steps per batch of B loads (two batches in flight)
 constexpr uint32_t kMultiVS = 130 * 8;  // one accumulator buffer: 128 outputs + spare (index 128)
 constexpr size_t kMultiWarpBytes = kMultiM * kMultiVS + 128 * 4 + 32 * 8 + kMultiM * 32 * 8 + 32 * 32 * 2;  // 7488
 static_assert(kMultiWarps * kMultiWarpBytes + 1024 < 65536, "the map holds 16-bit shared addresses");
@@ -168,9 +171,9 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
         for (int r = 0; r < M; ++r)
           for (int e = lane; e < n; e += G) vals[r * VD + e] = 0.0;  // accumulators from +0.0
         __syncwarp();
-#pragma unroll 1
-        for (int j0 = 0; j0 < na; j0 += U) {
-          double bv[U][M];
+        // B values of U steps x M rows; the next batch's loads are issued
+        // before this batch's folds (software pipeline, two register sets)
+        auto load = [&](int j0, double (&bv)[U][M]) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint2 bl = meta[j0 + u];  // rows j >= na: length 0
@@ -179,6 +182,8 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
             for (int r = 0; r < M; ++r)
               bv[u][r] = ldg_f64_if(bvl + static_cast<size_t>(bl.x + r * bl.y) * 8u, on && r < m);
           }
+        };
+        auto fold = [&](int j0, const double (&bv)[U][M]) {
           uint32_t am[U];  // the steps' map entries, loaded ahead of the chains
 #pragma unroll
           for (int u = 0; u < U; ++u) am[u] = mapl[(j0 + u) * G];
@@ -205,6 +210,16 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
 #pragma unroll
             for (int r = 0; r < M; ++r) sts_f64(a + r * kMultiVS, __dadd_rn(acc[r], x[u][r]));
           }
+        };
+        double bA[U][M], bB[U][M];
+        load(0, bA);
+#pragma unroll 1
+        for (int j0 = 0; j0 < na; j0 += 2 * U) {
+          if (j0 + U < na) load(j0 + U, bB);
+          fold(j0, bA);
+          if (j0 + U >= na) break;
+          if (j0 + 2 * U < na) load(j0 + 2 * U, bA);
+          fold(j0 + U, bB);
         }
         __syncwarp();
         // C rows: the previous row's columns + r + 1, buffer r's values
