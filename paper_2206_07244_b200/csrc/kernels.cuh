@@ -400,7 +400,22 @@ __global__ void __launch_bounds__(kBinThreads)
     const bool longrow = (a1 - a0) > 32;
     long long n = 0;
     if (!longrow) {
-      for (int64_t p = a0; p < a1; ++p) {
+      // 4 entries per round: their column loads, then their B-row bounds, in flight together
+      int64_t p = a0;
+      for (; p + 4 <= a1; p += 4) {
+        int32_t k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) k[u] = A.col[p + u];
+        long long l[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) l[u] = brpt[k[u] + 1] - brpt[k[u]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          n += l[u];
+          bmax = max(bmax, l[u]);
+        }
+      }
+      for (; p < a1; ++p) {
         const int32_t k = A.col[p];
         const long long l = brpt[k + 1] - brpt[k];
         n += l;
@@ -2644,8 +2659,20 @@ __global__ void __launch_bounds__(256)
     bool same = false;
     if (k > 0) {
       const int64_t r0 = B.rpt[k - 1], r1 = B.rpt[k], r2 = B.rpt[k + 1];
-      same = r2 - r1 == r1 - r0;
-      for (int64_t q = 0; same && q < r2 - r1; ++q) same = B.col[r1 + q] == B.col[r0 + q] + 1;
+      const int64_t len = r2 - r1;
+      same = len == r1 - r0;
+      // 8 entries per round, their loads issued before any is compared
+      for (int64_t q0 = 0; same && q0 < len; q0 += 8) {
+        int32_t c[8], cp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool on = q0 + u < len;
+          c[u] = on ? B.col[r1 + q0 + u] : 1;
+          cp[u] = on ? B.col[r0 + q0 + u] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) same = same && c[u] == cp[u] + 1;
+      }
     }
     shift1[k] = same ? 1 : 0;
   }

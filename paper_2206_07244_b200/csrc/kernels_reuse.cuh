@@ -75,6 +75,7 @@ constexpr int kMultiU = SPGEMM_MULTI_U;  // steps per batch of B loads (two batc
 constexpr uint32_t kMultiVS = 130 * 8;  // one accumulator buffer: 128 outputs + spare (index 128)
 constexpr size_t kMultiWarpBytes = kMultiM * kMultiVS + 128 * 4 + 32 * 8 + kMultiM * 32 * 8 + 32 * 32 * 2;  // 7488
 static_assert(kMultiWarps * kMultiWarpBytes + 1024 < 65536, "the map holds 16-bit shared addresses");
+static_assert(kMultiVS % 16 == 0 && kMultiWarpBytes % 16 == 0, "16-byte aligned accumulator buffers");
 static_assert(32 % kMultiU == 0 && kMultiU % 2 == 0, "U: even, divides the warp width");
 
 __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
@@ -167,9 +168,11 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
         // the group's A values: its rows are consecutive in A, na entries each
 #pragma unroll
         for (int r = 0; r < M; ++r) avs[r * 32 + lane] = (r < m && lane < na) ? A.val[a0 + r * na + lane] : 0.0;
+        // accumulators from +0.0 (pairs: a buffer is 16-byte aligned, VD even)
 #pragma unroll
         for (int r = 0; r < M; ++r)
-          for (int e = lane; e < n; e += G) vals[r * VD + e] = 0.0;  // accumulators from +0.0
+          for (int e = 2 * lane; e < n; e += 2 * G)
+            *reinterpret_cast<double2*>(vals + r * VD + e) = make_double2(0.0, 0.0);
         __syncwarp();
         // B values of U steps x M rows; the next batch's loads are issued
         // before this batch's folds (software pipeline, two register sets)

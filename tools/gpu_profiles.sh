@@ -32,7 +32,7 @@ for c in 2 1 4 3; do
     gpurun_out/${R}_ncu_full_config$c.md > /dev/null
   python tools/ncu_brief.py /tmp/ncu/${R}_full_config$c.ncu-rep > gpurun_out/${R}_ncu_brief_config$c.txt 2>&1
 done
-for k in k_num_reuse k_num_lean k_num_thread k_big_num_ord k_big_sym; do
+for k in k_num_reuse_multi k_sym_reuse k_reuse_flags k_num_lean k_num_thread k_big_num_ord k_big_sym; do
   for c in 2 4 1 3; do
     python tools/ncu_source.py /tmp/ncu/${R}_full_config$c.ncu-rep $k 30 > gpurun_out/${R}_src_${k}_config$c.txt 2>/dev/null
     [ -s gpurun_out/${R}_src_${k}_config$c.txt ] || rm -f gpurun_out/${R}_src_${k}_config$c.txt
