@@ -79,6 +79,7 @@ spgemm_status guard(F&& f) {
 // -------------------------------------------------------------- presets
 // binning.cpp:26-66 -- the same published ranges and capacities.
 constexpr int64_t kNoUpper = std::numeric_limits<int64_t>::max();
+constexpr int64_t kSharedNumMax = 8192;  // largest numeric row on chip (k_num_block<16384, 1024, 8192>)
 constexpr int64_t kSymTable[kNumBins] = {32, 512, 1024, 2048, 4096, 8192, 12287, 24575};
 constexpr int64_t kNumTable[kNumBins] = {31, 255, 511, 1023, 2047, 4095, 8191, 0};
 
@@ -487,6 +488,16 @@ struct spgemm_pipeline {
   bool square_like() const { return A.rows == B.rows && A.cols == B.cols && a_nnz == b_nnz; }
   bool heap_ordered() const { return opts.ordered_heap || opts.deterministic; }
   bool heap_bitmap() const { return idx32; }  // bitmap kernels (ordered or atomic); else k_num_global
+  // numeric bins past the largest on-chip table (16384 slots: rows of <= 8192
+  // nonzeros, the B200 tier) take the heap tier; so do the block-table bins
+  // whose rows all have > 2048 nonzeros when B's rows are short on average, as
+  // in the symbolic phase: a per-A-entry block walk leaves most threads idle on
+  // skewed graphs, the bitmap walk is balanced by products
+  bool heap_tier(int bin) const {
+    const int64_t u = num_plan.config.upper[bin];
+    const int64_t lo = bin > 0 ? num_plan.config.upper[bin - 1] + 1 : 0;
+    return bin == kNumBins - 1 || u > kSharedNumMax || (heap_bitmap() && lo > 2048 && avg_b_len < 64.0);
+  }
   int32_t* d_poff = nullptr;                   // ordered bitmap tier: B's column-panel offsets
   uint8_t* d_shift1 = nullptr;                 // B row k == B row k-1 shifted by one (arena)
   uint8_t* d_rflag = nullptr;                  // row i's structure == row i-1's shifted by one (arena)
@@ -902,25 +913,25 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     SPG_LAUNCH(ctx, "k_num_group<" + std::to_string(G) + "," + std::to_string(T) + ">", s,
                kern<<<grid, G * NGRP, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num, spec));
   };
-  auto block = [&](auto kern, int T, int threads, int nmax) {
-    const size_t smem = static_cast<size_t>(T) * 12 + static_cast<size_t>(nmax) * 8;
+  auto block = [&](auto kern, int T, int threads, int nmax, bool overlay = false) {
+    const size_t smem = static_cast<size_t>(T) * 12 + (overlay ? 0 : static_cast<size_t>(nmax) * 8);
     prepare_kernel(ctx, kern, smem);
     const int grid = persistent_grid(ctx, kern, threads, smem, rl.count);
     SPG_LAUNCH(ctx, "k_num_block<" + std::to_string(T) + ">", s,
                kern<<<grid, threads, smem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, d_info_num));
   };
-  if ((bin == kNumBins - 1 || u > 4096) && heap_bitmap() && heap_ordered()) {
+  if (heap_tier(bin) && heap_bitmap() && heap_ordered()) {
     prepare_kernel(ctx, k_big_num_ord, kBigNumSmem);
     const int grid = persistent_grid(ctx, k_big_num_ord, kBigThreads, kBigNumSmem, rl.count);
     SPG_LAUNCH(ctx, "k_big_num_ord", s,
                k_big_num_ord<<<grid, kBigThreads, kBigNumSmem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, d_poff,
                                                                     d_info_num));
-  } else if ((bin == kNumBins - 1 || u > 4096) && heap_bitmap()) {
+  } else if (heap_tier(bin) && heap_bitmap()) {
     prepare_kernel(ctx, k_big_num, kBigNumSmem);
     const int grid = persistent_grid(ctx, k_big_num, kBigThreads, kBigNumSmem, rl.count);
     SPG_LAUNCH(ctx, "k_big_num", s,
                k_big_num<<<grid, kBigThreads, kBigNumSmem, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, d_info_num));
-  } else if (bin == kNumBins - 1 || u > 4096) {
+  } else if (heap_tier(bin)) {
     SPG_LAUNCH(ctx, "k_num_global", s,
                k_num_global<<<gblocks, kGlobalThreads, 0, s>>>(rl, A, B, d_rpt, d_ccol, d_cval, scale, gkeys,
                                                     gvals, gbits, gslots, gwords, d_info_num));
@@ -971,8 +982,12 @@ void spgemm_pipeline::launch_num_bin(int bin, const RowList& rl, cudaStream_t s,
     block(k_num_block<2048, 256, 1024>, 2048, 256, 1024);
   } else if (u <= 2048) {
     block(k_num_block<4096, 256, 2048>, 4096, 256, 2048);
-  } else {
+  } else if (u <= 4096) {
     block(k_num_block<8192, 512, 4096>, 8192, 512, 4096);
+  } else {
+    // B200 tier: rows of 4097..8192 nonzeros (bin 6 of num_1x / num_1.5x, whose
+    // reference tier is a fixed table) stay on chip in a 16384-slot table
+    block(k_num_block<16384, 1024, 8192, true>, 16384, 1024, 8192, true);
   }
 }
 
@@ -982,7 +997,7 @@ void spgemm_pipeline::run_numeric() {
   // Global (heap) tier pool, sized from the exact max row nnz of pass 1.
   int64_t grows = 0;
   for (int j = 0; j < kNumBins; ++j)
-    if (j == kNumBins - 1 || num_plan.config.upper[j] > 4096) grows += bin_info.bin_size[j];
+    if (heap_tier(j)) grows += bin_info.bin_size[j];
   int32_t* gkeys = nullptr;
   double* gvals = nullptr;
   uint32_t* gbits = nullptr;
@@ -1036,7 +1051,7 @@ void spgemm_pipeline::run_numeric() {
     const int bin = num_plan.launch_order[r];
     if (bin_info.bin_size[bin] == 0) continue;
     // the heap-tier bins share the k_num_global pool: one stream for them
-    const bool heap_bin = bin == kNumBins - 1 || num_plan.config.upper[bin] > 4096;
+    const bool heap_bin = heap_tier(bin);
     cudaStream_t s = heap_bin && !heap_bitmap() ? ctx->main_s : bin_stream(ctx, bin);
     ck(cudaStreamWaitEvent(s, ctx->ev_fork, 0), "wait fork");
     RowList rl{d_bins, bin_info.bin_offset[bin], bin_info.bin_size[bin], bin_info.fast_path, nullptr, bin};

@@ -2700,16 +2700,22 @@ __device__ __forceinline__ void block_bitonic_smem(unsigned long long* a, int np
 
 // Block kernel: one row per block iteration, table of T slots in shared
 // memory, ordered steps with a block barrier per A entry.
-template <int T, int THREADS, int NMAX>
+// OVERLAY (the B200 tier for rows of up to 8192 nonzeros: T = 16384 slots,
+// 128 KB of values + 64 KB of keys): the sort keys overlay the table's keys --
+// the condense step reads every thread's slots into registers before the
+// block-wide scan, so the packed (column, slot) keys can be written over them;
+// 192 KB per block instead of 256 KB.
+template <int T, int THREADS, int NMAX, bool OVERLAY = false>
 __global__ void __launch_bounds__(THREADS)
     k_num_block(RowList rl_in, DevCsr A, DevCsr B, const int64_t* __restrict__ rpt,
                 int32_t* __restrict__ ccol, double* __restrict__ cval, uint32_t scale,
                 DevInfo* info) {
+  static_assert(!OVERLAY || NMAX * 8 <= T * 4, "the sort keys must fit the table's keys");
   const RowList rl = rl_in.resolved();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* vals = reinterpret_cast<double*>(smem_raw);
   unsigned long long* packed = reinterpret_cast<unsigned long long*>(smem_raw + T * 8);
-  int32_t* keys = reinterpret_cast<int32_t*>(smem_raw + T * 8 + NMAX * 8);
+  int32_t* keys = reinterpret_cast<int32_t*>(smem_raw + T * 8 + (OVERLAY ? 0 : NMAX * 8));
   __shared__ long long s_red[32];
   constexpr int PER = T / THREADS;
   const Hash hs = make_hash(scale, log2_const<T>());
@@ -2735,18 +2741,23 @@ __global__ void __launch_bounds__(THREADS)
       }
       __syncthreads();
     }
-    // condense: each thread owns PER consecutive slots
+    // condense: each thread owns PER consecutive slots (read into registers
+    // first: with OVERLAY the packed keys are written over the table's keys)
+    int32_t kv[PER];
     int mine = 0;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) mine += keys[threadIdx.x * PER + i] != -1;
+    for (int i = 0; i < PER; ++i) {
+      kv[i] = keys[threadIdx.x * PER + i];
+      mine += kv[i] != -1;
+    }
     long long total;
     long long pos = block_exclusive_scan<THREADS>(mine, s_red, &total);
+    if constexpr (OVERLAY) __syncthreads();  // every thread's slots read before any packed write
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int s = threadIdx.x * PER + i;
-      const int32_t key = keys[s];
-      if (key != -1)
-        packed[pos++] = (static_cast<unsigned long long>(static_cast<uint32_t>(key)) << 32) |
+      if (kv[i] != -1)
+        packed[pos++] = (static_cast<unsigned long long>(static_cast<uint32_t>(kv[i])) << 32) |
                         static_cast<uint32_t>(s);
     }
     if (threadIdx.x == 0 && total != n) atomicOr(&info->error, kErrNumericCount);

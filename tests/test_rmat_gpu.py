@@ -142,3 +142,29 @@ def test_rmat24_config5_sampled(sg, oracle):
     assert_matches_oracle(got.c, exp)
     del d
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("num", ["num_1x", "num_1.5x"])
+def test_b200_block_tier(sg, oracle, num):
+    """Bin 6 of num_1x / num_1.5x (4096..8191 / 3073..5460 nonzeros; a fixed-table
+    tier in the reference) runs on chip in the 16384-slot table
+    (k_num_block<16384>: sort keys over the table's keys, 192 KB of the B200's
+    227 KB per block) when B's rows are long; bitwise the reference."""
+    from helpers import random_csr_fixed
+    a = S.random_values(random_csr_fixed(300, 20000, 55, 51), 52)
+    b = S.random_values(random_csr_fixed(20000, 20000, 100, 53), 54)
+    exp = oracle.spgemm(a, b)
+    lens = np.diff(exp.rpt)
+    assert ((lens > 4096) & (lens <= 5460)).all()
+    ctx = sg.get_context()
+    ctx.set_profiling(True)
+    try:
+        ctx.profile_summary()
+        out = sg.multiply(a, b, sg.SpgemmOptions(num_preset=num))
+        names = ctx.profile_summary()
+    finally:
+        ctx.set_profiling(False)
+    assert_matches_oracle(out.c, exp)
+    assert any(k.split("#")[0] == "k_num_block<16384>" for k in names), sorted(names)
+    out = sg.multiply(a, b, sg.SpgemmOptions(num_preset=num, deterministic=False))
+    assert_matches_oracle(out.c, exp)  # an on-chip tier: ordered either way
