@@ -815,6 +815,19 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
 __device__ __forceinline__ void sts_f64(uint32_t a, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
 }
+// predicated shared-window f64 load / store (no access when !on)
+__device__ __forceinline__ double lds_f64_if(uint32_t a, bool on) {
+  double v = 0.0;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
+      : "+d"(v)
+      : "r"(a), "r"(static_cast<int>(on)));
+  return v;
+}
+__device__ __forceinline__ void sts_f64_if(uint32_t a, double v, bool on) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f64 [%0], %1;\n\t}" ::"r"(a),
+               "d"(v), "r"(static_cast<int>(on)));
+}
 // predicated read-only global f64 load (0.0 when !on)
 __device__ __forceinline__ double ldg_f64_if(const void* p, bool on) {
   double v = 0.0;

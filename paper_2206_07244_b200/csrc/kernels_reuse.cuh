@@ -72,8 +72,18 @@ constexpr int kMultiM = 4;               // flagged rows folded together
 #define SPGEMM_MULTI_U 2
 #endif
 constexpr int kMultiU = SPGEMM_MULTI_U;  // steps per batch of B loads (two batches in flight)
-constexpr uint32_t kMultiVS = 130 * 8;  // one accumulator buffer: 128 outputs + spare (index 128)
-constexpr size_t kMultiWarpBytes = kMultiM * kMultiVS + 128 * 4 + 32 * 8 + kMultiM * 32 * 8 + 32 * 32 * 2;  // 7488
+constexpr uint32_t kMultiVS = 152 * 8;  // one accumulator buffer: slots multi_slot(0..127) + spare (151)
+constexpr int kMultiSpare = 151;
+// Accumulator slot of output position p. 64-bit shared accesses are served per
+// half-warp: 16 lanes whose slots share a bank pair (slot mod 16) cost an extra
+// wavefront. Output positions of a 3-D stencil product come in planes of 25
+// (5 x 5 for radius 2), and a step's 27 products then collide mod 16 (2
+// wavefronts per half-warp); skewing every plane by 4 slots leaves 3
+// wavefronts per warp access instead of 4 (tools: DESIGN §6). Any permutation
+// is exact; this one only changes bank conflicts.
+__device__ __forceinline__ int multi_slot(int p) { return p + 4 * (p / 25); }
+static_assert(127 + 4 * (127 / 25) < kMultiSpare, "slots below the spare");
+constexpr size_t kMultiWarpBytes = kMultiM * kMultiVS + 128 * 4 + 32 * 8 + kMultiM * 32 * 8 + 32 * 32 * 2;  // 8704
 static_assert(kMultiWarps * kMultiWarpBytes + 1024 < 65536, "the map holds 16-bit shared addresses");
 static_assert(kMultiVS % 16 == 0 && kMultiWarpBytes % 16 == 0, "16-byte aligned accumulator buffers");
 static_assert(32 % kMultiU == 0 && kMultiU % 2 == 0, "U: even, divides the warp width");
@@ -168,25 +178,28 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
         // the group's A values: its rows are consecutive in A, na entries each
 #pragma unroll
         for (int r = 0; r < M; ++r) avs[r * 32 + lane] = (r < m && lane < na) ? A.val[a0 + r * na + lane] : 0.0;
-        // accumulators from +0.0 (pairs: a buffer is 16-byte aligned, VD even)
+        // accumulators from +0.0: every slot up to the last output's (pairs: a
+        // buffer is 16-byte aligned, VD even)
+        const int zn = multi_slot(n - 1) + 1;
 #pragma unroll
         for (int r = 0; r < M; ++r)
-          for (int e = 2 * lane; e < n; e += 2 * G)
+          for (int e = 2 * lane; e < zn; e += 2 * G)
             *reinterpret_cast<double2*>(vals + r * VD + e) = make_double2(0.0, 0.0);
         __syncwarp();
         // B values of U steps x M rows; the next batch's loads are issued
         // before this batch's folds (software pipeline, two register sets)
-        auto load = [&](int j0, double (&bv)[U][M]) {
+        auto load = [&](int j0, double (&bv)[U][M], bool (&on_)[U]) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint2 bl = meta[j0 + u];  // rows j >= na: length 0
             const bool on = lane < static_cast<int>(bl.y);
+            on_[u] = on;
 #pragma unroll
             for (int r = 0; r < M; ++r)
               bv[u][r] = ldg_f64_if(bvl + static_cast<size_t>(bl.x + r * bl.y) * 8u, on && r < m);
           }
         };
-        auto fold = [&](int j0, const double (&bv)[U][M]) {
+        auto fold = [&](int j0, const double (&bv)[U][M], const bool (&on)[U]) {
           uint32_t am[U];  // the steps' map entries, loaded ahead of the chains
 #pragma unroll
           for (int u = 0; u < U; ++u) am[u] = mapl[(j0 + u) * G];
@@ -202,27 +215,29 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            // lanes without a product (lane >= len, j >= na) fold into the spare
-            // slot. The volatile shared accesses stay in program order: the M
+            // lanes without a product (lane >= len, j >= na) are predicated off
+            // (no shared access: a common spare slot would add a wavefront).
+            // The volatile shared accesses stay in program order: the M
             // buffers' loads of step u, then their stores -- the M chains
             // overlap, and step u's stores precede step u+1's loads
             const uint32_t a = am[u];
             double acc[M];
 #pragma unroll
-            for (int r = 0; r < M; ++r) acc[r] = lds_f64(a + r * kMultiVS);
+            for (int r = 0; r < M; ++r) acc[r] = lds_f64_if(a + r * kMultiVS, on[u]);
 #pragma unroll
-            for (int r = 0; r < M; ++r) sts_f64(a + r * kMultiVS, __dadd_rn(acc[r], x[u][r]));
+            for (int r = 0; r < M; ++r) sts_f64_if(a + r * kMultiVS, __dadd_rn(acc[r], x[u][r]), on[u]);
           }
         };
         double bA[U][M], bB[U][M];
-        load(0, bA);
+        bool oA[U], oB[U];
+        load(0, bA, oA);
 #pragma unroll 1
         for (int j0 = 0; j0 < na; j0 += 2 * U) {
-          if (j0 + U < na) load(j0 + U, bB);
-          fold(j0, bA);
+          if (j0 + U < na) load(j0 + U, bB, oB);
+          fold(j0, bA, oA);
           if (j0 + U >= na) break;
-          if (j0 + 2 * U < na) load(j0 + 2 * U, bA);
-          fold(j0 + U, bB);
+          if (j0 + 2 * U < na) load(j0 + 2 * U, bA, oA);
+          fold(j0 + U, bB, oB);
         }
         __syncwarp();
         // C rows: the previous row's columns + r + 1, buffer r's values
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
           for (int r = 0; r < M; ++r) {
             if (r < m) {
               ccol[rb[r] + e] = c0 + r + 1;
-              cval[rb[r] + e] = vals[r * VD + e];
+              cval[rb[r] + e] = vals[r * VD + multi_slot(e)];
             }
           }
           ocols[e] = c0 + m;
@@ -277,7 +292,7 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
       if (reused) {
         // same shape at shift d: check every product's column while folding
         bool ok = true;
-        for (int e = lane; e < n; e += G) vals[e] = 0.0;
+        for (int e = lane; e <= multi_slot(n - 1); e += G) vals[e] = 0.0;
         __syncwarp();
         for (int j = 0; j < na; ++j) {
           const int32_t pbj = __shfl_sync(kFull, pb0, j);
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
           const int32_t c = ocols[e] + d;
           ocols[e] = c;
           ocp[e] = c;
-          ovp[e] = vals[e];
+          ovp[e] = vals[multi_slot(e)];
         }
         ++nreuse;
       } else {
@@ -395,8 +410,8 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
         // rows; map rows j >= na and lanes past a B row's length: the spare slot
         for (int j = 0; j < G; ++j) {
           const int lj = __shfl_sync(kFull, len, j);
-          map[j * G + lane] =
-              static_cast<uint16_t>(vals_sa + 8u * ((j < na && lane < lj) ? rank[map[j * G + lane]] : NMAX));
+          map[j * G + lane] = static_cast<uint16_t>(
+              vals_sa + 8u * ((j < na && lane < lj) ? multi_slot(rank[map[j * G + lane]]) : kMultiSpare));
         }
         __syncwarp();
         ++nfull;
