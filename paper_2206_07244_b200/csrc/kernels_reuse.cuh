@@ -178,14 +178,8 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
         // the group's A values: its rows are consecutive in A, na entries each
 #pragma unroll
         for (int r = 0; r < M; ++r) avs[r * 32 + lane] = (r < m && lane < na) ? A.val[a0 + r * na + lane] : 0.0;
-        // accumulators from +0.0: every slot up to the last output's (pairs: a
-        // buffer is 16-byte aligned, VD even)
-        const int zn = multi_slot(n - 1) + 1;
-#pragma unroll
-        for (int r = 0; r < M; ++r)
-          for (int e = 2 * lane; e < zn; e += 2 * G)
-            *reinterpret_cast<double2*>(vals + r * VD + e) = make_double2(0.0, 0.0);
-        __syncwarp();
+        // (no zeroing: a position's first product in A order -- bit 0 of its map
+        // entry -- is stored as 0.0 + x without reading the accumulator)
         // B values of U steps x M rows; the next batch's loads are issued
         // before this batch's folds (software pipeline, two register sets)
         auto load = [&](int j0, double (&bv)[U][M], bool (&on_)[U]) {
@@ -220,10 +214,11 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
             // The volatile shared accesses stay in program order: the M
             // buffers' loads of step u, then their stores -- the M chains
             // overlap, and step u's stores precede step u+1's loads
-            const uint32_t a = am[u];
+            const uint32_t a = am[u] & ~1u;
+            const bool rd = on[u] && (am[u] & 1u) == 0u;  // not the position's first product
             double acc[M];
 #pragma unroll
-            for (int r = 0; r < M; ++r) acc[r] = lds_f64_if(a + r * kMultiVS, on[u]);
+            for (int r = 0; r < M; ++r) acc[r] = lds_f64_if(a + r * kMultiVS, rd);  // 0.0 when not read
 #pragma unroll
             for (int r = 0; r < M; ++r) sts_f64_if(a + r * kMultiVS, __dadd_rn(acc[r], x[u][r]), on[u]);
           }
@@ -292,8 +287,6 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
       if (reused) {
         // same shape at shift d: check every product's column while folding
         bool ok = true;
-        for (int e = lane; e <= multi_slot(n - 1); e += G) vals[e] = 0.0;
-        __syncwarp();
         for (int j = 0; j < na; ++j) {
           const int32_t pbj = __shfl_sync(kFull, pb0, j);
           const uint2 mj = meta[j];
@@ -303,7 +296,8 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
             const double x = __dmul_rn(avs[j], B.val[mj.x + lane]);
             ok = ok && c - cp == d;
             const uint32_t a = map[j * G + lane];
-            sts_f64(a, __dadd_rn(lds_f64(a), x));
+            const uint32_t aa = a & ~1u;
+            sts_f64(aa, __dadd_rn((a & 1u) ? 0.0 : lds_f64(aa), x));
           }
           __syncwarp();
           if (!__all_sync(kFull, ok)) break;  // structure differs: the full path recomputes
@@ -408,12 +402,22 @@ __global__ void __launch_bounds__(32 * kMultiWarps, SPGEMM_MULTI_MINB)
         __syncwarp();
         // product -> its output's accumulator address (buffer 0) for the next
         // rows; map rows j >= na and lanes past a B row's length: the spare slot
+        // bit 0: the product is its position's first in A order (the claim-order
+        // columns are consumed: their bytes mark the positions seen)
+        uint8_t* seen = reinterpret_cast<uint8_t*>(cols);
+        for (int e = lane; e < NMAX; e += G) seen[e] = 0;
+        __syncwarp();
         for (int j = 0; j < G; ++j) {
           const int lj = __shfl_sync(kFull, len, j);
-          map[j * G + lane] = static_cast<uint16_t>(
-              vals_sa + 8u * ((j < na && lane < lj) ? multi_slot(rank[map[j * G + lane]]) : kMultiSpare));
+          uint32_t m = vals_sa + 8u * kMultiSpare;
+          if (j < na && lane < lj) {
+            const int pos = rank[map[j * G + lane]];
+            m = vals_sa + 8u * multi_slot(pos) + (seen[pos] ? 0u : 1u);
+            seen[pos] = 1;  // (a step's positions are distinct)
+          }
+          map[j * G + lane] = static_cast<uint16_t>(m);
+          __syncwarp();
         }
-        __syncwarp();
         ++nfull;
       }
       pvalid = true;
