@@ -23,9 +23,14 @@
 // A-row order from +0.0 -- bitwise the reference (hash_tables.cpp:179-201,
 // reference.cpp:21-27). The M read-modify-write chains are independent, so
 // the shared-memory latency of one chain (ld -> add -> st -> next ld) is
-// hidden by the other M-1, and the U steps' M*U B values are loaded together.
+// hidden by the other M-1; the next batch's B values are loaded while this
+// batch folds. The kernel is bound by the L1 data pipe (ncu: ~90% of peak,
+// two thirds of it the accumulators' shared loads and stores), so the layout
+// minimises shared wavefronts: accumulator slots skewed per 25-position plane
+// (multi_slot: fewer bank conflicts), lanes without a product predicated off,
+// and each position's first product stored without a read (no zeroing).
 // (k_num_reuse folds one row at a time: its single chain left the warp
-// stalled on shared memory; ncu, DESIGN §10.)
+// stalled on shared memory; ncu, DESIGN §6.)
 #pragma once
 
 namespace spgemm_b200 {
