@@ -2606,24 +2606,45 @@ __global__ void __launch_bounds__(32 * kSymReuseWarps)
         }
         __syncwarp();
         int cnt = 0;
-        for (int j = 0; j < hna; ++j) {
-          const int64_t q1 = __shfl_sync(kFull, hb1, j);
-          for (int64_t q = __shfl_sync(kFull, hb0, j) + lane; q < q1; q += G) {
-            const int32_t c = B.col[q];
-            uint32_t hh = (static_cast<uint32_t>(c) * mult) >> hshift;
-            int32_t cur = keys[hh];
-            while (cur != c) {
+        auto insert = [&](int32_t c) {
+          uint32_t hh = (static_cast<uint32_t>(c) * mult) >> hshift;
+          int32_t cur = keys[hh];
+          while (cur != c) {
+            if (cur == -1) {
+              cur = atomicCAS(reinterpret_cast<int*>(keys + hh), -1, c);
               if (cur == -1) {
-                cur = atomicCAS(reinterpret_cast<int*>(keys + hh), -1, c);
-                if (cur == -1) {
-                  ++cnt;
-                  break;
-                }
-              } else {
-                hh = (hh + 1) & hmask;
-                cur = *reinterpret_cast<volatile int32_t*>(keys + hh);
+                ++cnt;
+                break;
               }
+            } else {
+              hh = (hh + 1) & hmask;
+              cur = *reinterpret_cast<volatile int32_t*>(keys + hh);
             }
+          }
+        };
+        const int hlen = static_cast<int>(hb1 - hb0);
+        if (__reduce_max_sync(kFull, static_cast<unsigned>(hlen)) <= static_cast<unsigned>(G) &&
+            __shfl_sync(kFull, hb1, max(hna - 1, 0)) < (int64_t(1) << 31)) {
+          // B rows of <= 32 entries (the route's rows): 8 entries' columns loaded
+          // before any is inserted (one latency per 8 entries, not per entry)
+          const int32_t hb = static_cast<int32_t>(hb0);
+          for (int j0 = 0; j0 < hna; j0 += 8) {
+            int32_t c[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = (j0 + u) & 31;
+              const int32_t bj = __shfl_sync(kFull, hb, j);
+              const int lj = __shfl_sync(kFull, hlen, j);
+              c[u] = (j0 + u < hna && lane < lj) ? B.col[bj + lane] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (c[u] >= 0) insert(c[u]);
+          }
+        } else {
+          for (int j = 0; j < hna; ++j) {
+            const int64_t q1 = __shfl_sync(kFull, hb1, j);
+            for (int64_t q = __shfl_sync(kFull, hb0, j) + lane; q < q1; q += G) insert(B.col[q]);
           }
         }
         cnt_total = static_cast<long long>(__reduce_add_sync(kFull, static_cast<unsigned>(cnt)));
