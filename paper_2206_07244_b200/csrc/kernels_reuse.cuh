@@ -56,11 +56,13 @@ __global__ void __launch_bounds__(256)
           c[u] = on ? A.col[r1 + q0 + u] : 0;
           cp[u] = on && !a_is_b ? A.col[r0 + q0 + u] : c[u] - 1;
         }
+        // the 8 flag gathers issued together (no short-circuit between them)
+        uint8_t sf[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sf[u] = q0 + u < na ? shift1[c[u]] : uint8_t{1};
         bool f = true;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (q0 + u < na) f = f && c[u] == cp[u] + 1 && shift1[c[u]] != 0;
-        }
+        for (int u = 0; u < 8; ++u) f = f & (q0 + u >= na || c[u] == cp[u] + 1) & (sf[u] != 0);
         ok = f;
       }
     }
