@@ -595,9 +595,10 @@ void spgemm_pipeline::setup() {
   off = align_up(off + static_cast<size_t>(std::max<int64_t>(M, 1)) * 8, 256);
   regular_a = M > 0 && static_cast<double>(h_sym.a_max_row) <= 4.0 * static_cast<double>(a_nnz) / static_cast<double>(M);
   // Structure-reuse route: A*A-shaped products of regular A with warp-sized A
-  // and B rows and B rows of > 8 entries on average (3-D stencils, FEM). The
-  // symbolic phase counts with k_sym_reuse, the numeric phase writes C with
-  // k_num_reuse -- no speculative scratch, no copy. SPGEMM_NO_REUSE=1 disables it.
+  // and B rows and B rows of > 8 entries on average (3-D stencils, FEM). Per-row
+  // flags (k_reuse_flags) drive the symbolic count (k_sym_reuse) and the
+  // numeric phase writes C with k_num_reuse_multi (kernels_reuse.cuh) -- no
+  // speculative scratch, no copy. SPGEMM_NO_REUSE=1 disables it.
   reuse_route = idx32 && M > 0 && h_sym.a_max_row <= 32 && h_sym.b_max_row <= 32 && regular_a &&
                 avg_b_len > 8.0 && square_like() && std::getenv("SPGEMM_NO_REUSE") == nullptr;
   const bool use_spec = !reuse_route && idx32 && M > 0 && avg_b_len > 8.0 && regular_a &&

@@ -2182,8 +2182,10 @@ __global__ void __launch_bounds__(32 * kPairWarps, 4)
   }
 }
 
-// Structure-reuse numeric for warp-sized rows (3-D stencils, FEM, the RAP
-// chain). One warp per row, a warp takes kReuseRows consecutive rows of its bin.
+// Structure-reuse numeric for warp-sized rows, one row at a time: the
+// speculative numeric of the symbolic phase (SPEC) for C = A*A-shaped products
+// outside the reuse route; the reuse route itself runs k_num_reuse_multi
+// (kernels_reuse.cuh). One warp per row, a warp takes kReuseRows consecutive rows of its bin.
 // Row i's output STRUCTURE is that of the warp's previous row i' shifted by
 // d = k_1(i) - k_1(i') exactly when both rows have the same number of A
 // entries, entry j's B rows have the same length, and every product column
