@@ -626,11 +626,11 @@ void spgemm_pipeline::setup() {
   d_rflag = nullptr;
   if (use_shift && b_rows > 0) {
     d_shift1 = d_arena + o_shift;
-    const int fg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(b_rows, 256)));
+    const int fg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 64, ceil_div(b_rows, 256)));
     SPG_LAUNCH(ctx, "k_shift_flags", s, k_shift_flags<<<std::max(fg, 1), 256, 0, s>>>(B, d_shift1));
     d_rflag = d_arena + o_rflag;
     const int a_is_b = A.rpt == B.rpt && A.col == B.col;
-    const int rg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, ceil_div(M, 256)));
+    const int rg = static_cast<int>(std::min<int64_t>(ctx->num_sms * 64, ceil_div(M, 256)));
     SPG_LAUNCH(ctx, "k_reuse_flags", s, k_reuse_flags<<<std::max(rg, 1), 256, 0, s>>>(A, d_shift1, d_rflag, a_is_b));
   }
   if (use_spec) {

@@ -2697,18 +2697,21 @@ __global__ void __launch_bounds__(256)
       const int64_t r0 = B.rpt[k - 1], r1 = B.rpt[k], r2 = B.rpt[k + 1];
       const int64_t len = r2 - r1;
       same = len == r1 - r0;
-      // 8 entries per round, their loads issued before any is compared
-      for (int64_t q0 = 0; same && q0 < len; q0 += 8) {
-        int32_t c[8], cp[8];
+      // 16 entries per round, their loads issued before any is compared (rows
+      // of <= 32 entries: at most two rounds, the second not waiting on the first)
+      bool ok = same;
+      for (int64_t q0 = 0; same && q0 < len; q0 += 16) {
+        int32_t c[16], cp[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {
           const bool on = q0 + u < len;
           c[u] = on ? B.col[r1 + q0 + u] : 1;
           cp[u] = on ? B.col[r0 + q0 + u] : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) same = same && c[u] == cp[u] + 1;
+        for (int u = 0; u < 16; ++u) ok = ok & (c[u] == cp[u] + 1);
       }
+      same = ok;
     }
     shift1[k] = same ? 1 : 0;
   }
